@@ -1,0 +1,339 @@
+#!/usr/bin/env python3
+"""Benchmark: GUP/s of the 512^3 x 496-view voxel-driven FDK backprojection
+(BASELINE.json metric, config 3) on B200, next to the reference CPU path.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--l 512]
+
+A "step" = one complete reconstruction (all 496 views) of the L^3 volume.
+  value      : nominal GUP/s (views * L^3 / s) with the projections resident in HBM,
+               CUDA-event time on the library's compute stream, max over ranks.
+  e2e        : the same metric through the public C ABI streaming call
+               (bp_gpu_backproject_async from pinned host memory + bp_gpu_finish into a
+               pinned host volume): H2D of every view and D2H of the volume are inside
+               the timed region.  Host wall clock around the API calls.
+  roofline   : binding roofline of the dominant kernel = shared-memory load bandwidth
+               (16 B of texel loads per VISIBLE voxel update).
+  cpu_baseline: the reference's own bp::reconstruct (oracle/_ref, built from
+               /root/reference sources) on a bounded sample of the workload.
+Inputs are seeded synthetic (BASELINE.json configs).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+METRIC = "GUP/s (voxel updates/s) for 512^3x496-view backprojection"
+SMEM_BYTES_PER_SM_CLK = 128.0
+N_SM = 148
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f)
+    except Exception:
+        return {}
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.device}", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, smax, reasons = [], None, set()
+        names = ["active", "hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown",
+                 "sw_power_cap"]
+        for ln in self.lines:
+            p = [x.strip() for x in ln.split(",")]
+            if len(p) < 9:
+                continue
+            try:
+                sm.append(float(p[1]))
+                smax = float(p[2])
+            except ValueError:
+                continue
+            for nm, v in zip(names[1:], p[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": smax,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def make_stack(args):
+    import paper_1104_5243_b200 as bp
+    t0 = time.time()
+    s = bp.Stack.baseline(n_views=args.views, isx=1248, isy=960, seed=args.seed)
+    return s, time.time() - t0
+
+
+# ---------------------------------------------------------------------------
+# reference arm: the reference's own CPU implementation (oracle/_ref)
+
+def cpu_reference_run(px, mats, L, sample_views, threads):
+    """bp::reconstruct of the reference (lanes 8, block_b 8, clip on, exact), BASELINE.md 3."""
+    from oracle import oracle as O
+    if O.ref() is not None:
+        sub_px, sub_m = px[:sample_views], mats[:sample_views]
+        t0 = time.time()
+        vol, st = O.ref_reconstruct(sub_px, sub_m, L, threads=threads, lanes=8, block_b=8,
+                                    clip=True)
+        wall = time.time() - t0
+        nominal = sample_views * L ** 3
+        return {"kind": "reference", "value": nominal / wall / 1e9, "wall_s": wall,
+                "timed_region_s": st["seconds"], "performed_updates": st["voxel_updates"],
+                "nominal_updates": nominal}
+    # oracle port (the reference could not be built here)
+    sub_px, sub_m = px[:sample_views], mats[:sample_views]
+    t0 = time.time()
+    O.reconstruct(sub_px, sub_m, L, threads=threads)
+    wall = time.time() - t0
+    nominal = sample_views * L ** 3
+    return {"kind": "port", "value": nominal / wall / 1e9, "wall_s": wall,
+            "nominal_updates": nominal}
+
+
+def run_reference_arm(args):
+    rank, world, local = dist_env()
+    if rank != 0:
+        return 0
+    import paper_1104_5243_b200 as bp  # datagen only (identical inputs to our arm)
+    stack, gen_s = make_stack(args)
+    px, mats = stack.pixels, stack.matrices
+    threads = os.cpu_count() or 1
+    L = args.l
+    sample = args.cpu_views
+    for _ in range(args.warmup):
+        cpu_reference_run(px, mats, L, max(1, sample // 4), threads)
+    vals, walls = [], []
+    for _ in range(args.steps):
+        r = cpu_reference_run(px, mats, L, sample, threads)
+        vals.append(r["value"])
+        walls.append(r["wall_s"])
+    v = float(np.median(vals))
+    ms_per_step = float(np.median(walls)) * 1e3 * (args.views / sample)
+    line = {
+        "metric": METRIC, "value": v, "unit": "GUP/s", "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "impl": "reference",
+        "config": {"workload": f"{L}^3 x {args.views} views of 1248x960, config 3", "l": L,
+                   "views": args.views, "sample_views": sample},
+        "cpu_baseline": {"value": v, "unit": "GUP/s", "cores": threads, "kind": r["kind"],
+                         "sample": f"{sample} of {args.views} views, full {L}^3 volume; "
+                                   "ms_per_step extrapolated to all views"},
+        "e2e": {"value": v, "unit": "GUP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------------------
+# our arm
+
+def run_ours(args):
+    import paper_1104_5243_b200 as bp
+    rank, world, local = dist_env()
+    dist = None
+    if world > 1:
+        import torch.distributed as dist  # plumbing only: barrier + max-reduce of timings
+        dist.init_process_group("gloo")
+    n_dev = bp.device_count()
+    if n_dev < 1:
+        print(json.dumps({"metric": METRIC, "error": "no CUDA device"}))
+        return 1
+    device = local % n_dev
+    L = args.l
+    stack, gen_s = make_stack(args)
+    px, mats = stack.pixels, stack.matrices
+    n, isy, isx = px.shape
+
+    # slab of this rank (work-balanced partition, identical on every rank)
+    if world > 1:
+        bounds = bp.partition_slabs(mats, isx, isy, L, world)
+        z0, z1 = int(bounds[rank]), int(bounds[rank + 1])
+    else:
+        z0, z1 = 0, L
+    nz = z1 - z0
+
+    # ---- visible updates (clip_stats semantics) for the roofline -------------
+    with bp.GpuContext(L, isx, isy, device=device, z_begin=z0, z_end=z1, count_visible=True,
+                       view_batch=args.batch, ring_batches=3) as c:
+        c.backproject_stack(stack)
+        _, vst = c.finish(readback=False)
+    visible = int(vst.visible_updates)
+
+    # ---- value: resident projections, device-event timing ---------------------
+    ring = (n + args.batch - 1) // args.batch
+    ctx = bp.GpuContext(L, isx, isy, device=device, z_begin=z0, z_end=z1, strict=args.strict,
+                        view_batch=args.batch, ring_batches=ring, profile_launches=True)
+    ctx.upload_stack(stack)
+    if args.warmup:
+        ctx.time_resident(args.warmup)
+    if dist:
+        dist.barrier()
+    clk = ClockSampler(device)
+    clk.start()
+    ms, st = ctx.time_resident(args.steps)
+    clocks = clk.stop()
+    if dist:
+        import torch
+        t = torch.tensor([ms], dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    nominal_step = n * L ** 3  # whole job, all ranks
+    value = nominal_step * args.steps / (ms / 1e3) / 1e9
+    launches = int(st.launches)
+    kernel_ms = float(st.kernel_ms)
+    per_launch_s = kernel_ms / 1e3 / max(1, launches)
+    ctx.close()
+
+    # ---- e2e: streamed through the C ABI from pinned host memory ---------------
+    e2e_ctx = bp.GpuContext(L, isx, isy, device=device, z_begin=z0, z_end=z1,
+                            strict=args.strict, view_batch=args.batch, ring_batches=3)
+    host_vol = bp.Volume.create(L)  # pinned (library pool)
+    out = host_vol.data[z0:z1]
+    for _ in range(max(1, args.warmup)):
+        e2e_ctx.backproject_stack(stack)
+        e2e_ctx.finish(out=out)
+    if dist:
+        dist.barrier()
+    t0 = time.perf_counter()
+    h2d = d2h = 0
+    for _ in range(args.steps):
+        e2e_ctx.backproject_stack(stack)
+        _, est = e2e_ctx.finish(out=out)
+        h2d += est.h2d_bytes
+        d2h += est.d2h_bytes
+    e2e_s = time.perf_counter() - t0
+    if dist:
+        import torch
+        t = torch.tensor([e2e_s], dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    e2e_ctx.close()
+    e2e_val = nominal_step * args.steps / e2e_s / 1e9
+
+    # ---- CPU baseline (rank 0, N=1 only) ----------------------------------------
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        threads = os.cpu_count() or 1
+        r = cpu_reference_run(px, mats, L, args.cpu_views, threads)
+        cpu = {"value": r["value"], "unit": "GUP/s", "cores": threads, "kind": r["kind"],
+               "sample": f"{args.cpu_views} of {n} views over the full {L}^3 volume "
+                         f"(bp::reconstruct lanes=8 block_b=8 clip=1; wall {r['wall_s']:.2f} s)"}
+
+    if rank != 0:
+        return 0
+    peaks = load_peaks()
+    sm_mhz = clocks.get("sm_mhz") or peaks.get("sm_max_mhz", 1965.0)
+    sm_max = clocks.get("sm_max_mhz") or peaks.get("sm_max_mhz", 1965.0)
+    # dominant kernel: tiled backprojection.  Algorithmic SMEM-load bytes per launch =
+    # 16 B x visible updates per launch (4 fp32 texels per update).
+    vis_per_launch = visible * world / max(1, (launches / args.steps))
+    achieved = 16.0 * (visible / max(1, launches / args.steps)) / per_launch_s / 1e9 if world == 1 \
+        else 16.0 * vis_per_launch / per_launch_s / 1e9
+    peak_nominal = SMEM_BYTES_PER_SM_CLK * N_SM * float(sm_max) * 1e6 / 1e9
+    line = {
+        "metric": METRIC, "value": value, "unit": "GUP/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": f"{L}^3 x {n} views of 1248x960 (BASELINE config 3)", "l": L,
+                   "views": n, "view_batch": args.batch,
+                   "arithmetic": "fast (FMA lerp)" if not args.strict else "strict (bitwise)",
+                   "l2": "inputs larger than L2 (2.38 GB stack + 512 MiB volume)",
+                   "parallelism": f"z-slab x{world}"},
+        "gpu_launches": launches,
+        "visible_updates_per_step": visible * (world if world > 1 else 1),
+        "gups_visible": visible * args.steps / (ms / 1e3) / 1e9,
+        "kernel_ms_per_step": kernel_ms / args.steps,
+        "roofline": {"bound": "smem", "achieved": achieved, "peak": peak_nominal,
+                     "unit": "GB/s", "frac": achieved / peak_nominal,
+                     "traffic": None,
+                     "peak_source": f"nominal 128 B/clk/SM x 148 SMs at sm_max {sm_max:.0f} MHz",
+                     "frac_at_measured_clock": achieved / (peak_nominal * float(sm_mhz) / float(sm_max))},
+        "e2e": {"value": e2e_val, "unit": "GUP/s", "h2d_bytes_per_step": h2d // args.steps,
+                "d2h_bytes_per_step": d2h // args.steps,
+                "ms_per_step": e2e_s * 1e3 / args.steps},
+        "clocks": clocks,
+        "tile": {"w": st.tile_w, "h": st.tile_h, "block": [st.block_x, st.block_y, st.block_z],
+                 "tile_pairs": st.tile_pairs, "skipped_pairs": st.skipped_pairs,
+                 "fallback_pairs": st.fallback_pairs},
+        "datagen_s": gen_s,
+    }
+    if cpu:
+        line["cpu_baseline"] = cpu
+    print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--l", type=int, default=512)
+    ap.add_argument("--views", type=int, default=496)
+    ap.add_argument("--batch", type=int, default=32)
+    ap.add_argument("--seed", type=int, default=20110428)
+    ap.add_argument("--strict", action="store_true", help="bitwise reference arithmetic")
+    ap.add_argument("--cpu-views", type=int, default=8)
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    args.fast_off = args.strict
+    if args.impl == "reference":
+        return run_reference_arm(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

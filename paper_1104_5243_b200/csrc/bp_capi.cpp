@@ -1,0 +1,588 @@
+// bp_capi.cpp -- extern "C" surface: include/backproject.h (reference-compatible)
+// and include/bp_gpu.h (streaming module ABI).
+//
+// Error behaviour follows proj/src/capi.cpp:18-39: exceptions never cross the
+// ABI; config_error -> BP_EINVAL, io_error -> BP_EIO, validation_error ->
+// BP_EVERIFY, everything else (CUDA failures included) -> BP_EINTERNAL, with a
+// thread-local message in bp_last_error().
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <thread>
+#include <tuple>
+#include <vector>
+
+#include "../../include/backproject.h"
+#include "../../include/bp_gpu.h"
+#include "bp_host.hpp"
+#include "bp_runtime.hpp"
+
+namespace {
+
+thread_local std::string g_last_error;
+
+int fail(int code, const std::string& msg) {
+    g_last_error = msg;
+    return code;
+}
+
+template <typename Fn>
+int guarded(Fn&& fn) {
+    try {
+        fn();
+        return BP_OK;
+    } catch (const bph::config_error& e) {
+        return fail(BP_EINVAL, e.what());
+    } catch (const bph::io_error& e) {
+        return fail(BP_EIO, e.what());
+    } catch (const bph::validation_error& e) {
+        return fail(BP_EVERIFY, e.what());
+    } catch (const std::exception& e) {
+        return fail(BP_EINTERNAL, e.what());
+    }
+}
+
+// ---- persistent device contexts ("loaded module") -------------------------
+// bp_reconstruct keeps one SlabContext per (device, geometry, slab, options)
+// alive between calls so that repeated reconstructions pay neither cudaMalloc
+// of the volume / projection ring nor stream creation.
+using CtxKey = std::tuple<int, uint32_t, uint32_t, uint32_t, double, double, double, int, int, int,
+                          int, int, int, int, int, int>;
+
+struct CtxCache {
+    std::mutex mu;
+    std::map<CtxKey, std::vector<std::unique_ptr<bpr::SlabContext>>> idle;
+};
+CtxCache& cache() {
+    static CtxCache* c = new CtxCache();
+    return *c;
+}
+
+CtxKey key_of(const bp_gpu_config& c) {
+    return CtxKey{c.device,        c.l,           c.isx,         c.isy,        c.offset_mm[0],
+                  c.offset_mm[1],  c.offset_mm[2], c.z_begin,     c.z_end,      c.view_batch,
+                  c.strict_mode,   c.distance_weight, c.row_windows, c.kernel, c.count_visible,
+                  c.recip_mode};
+}
+
+std::unique_ptr<bpr::SlabContext> acquire(const bp_gpu_config& c) {
+    {
+        auto& C = cache();
+        std::lock_guard<std::mutex> g(C.mu);
+        auto it = C.idle.find(key_of(c));
+        if (it != C.idle.end() && !it->second.empty()) {
+            auto p = std::move(it->second.back());
+            it->second.pop_back();
+            return p;
+        }
+    }
+    return std::make_unique<bpr::SlabContext>(c);
+}
+
+void release(std::unique_ptr<bpr::SlabContext> p) {
+    auto& C = cache();
+    std::lock_guard<std::mutex> g(C.mu);
+    auto& v = C.idle[key_of(p->config())];
+    if (v.size() < 2) v.push_back(std::move(p));
+}
+
+std::mutex g_dev_mu;
+std::vector<int> g_devices = {0};
+
+}  // namespace
+
+struct bp_stack {
+    bph::Stack s;
+};
+struct bp_volume {
+    bph::Volume v;
+};
+struct bp_gpu_ctx {
+    std::unique_ptr<bpr::SlabContext> c;
+};
+struct bp_machine {
+    int unused;
+};
+
+extern "C" {
+
+const char* bp_last_error(void) { return g_last_error.c_str(); }
+
+const char* bp_build_info(void) {
+    return "paper_1104_5243_b200 libbackproject: sm_100a tiled TMA backprojection "
+           "(packed FP32x2, strict/fast), built " __DATE__ " " __TIME__;
+}
+
+// ---- stacks ---------------------------------------------------------------
+
+int bp_stack_generate(const bp_gen_params* p, bp_stack** out) {
+    if (!p || !out) return fail(BP_EINVAL, "null argument");
+    return guarded([&] {
+        const double sid = p->sid_mm > 0 ? p->sid_mm : 750.0;
+        const double sdd = p->sdd_mm > 0 ? p->sdd_mm : 1200.0;
+        const double pitch = p->pitch_mm > 0 ? p->pitch_mm : 0.32;
+        const auto ph = bph::named_phantom(p->phantom ? p->phantom : "spheres3");
+        auto mats = bph::circular_trajectory(p->n_views, sid, sdd, p->isx, p->isy, pitch);
+        auto st = std::make_unique<bp_stack>();
+        st->s.isx = p->isx;
+        st->s.isy = p->isy;
+        st->s.mats = std::move(mats);
+        st->s.pixels = bph::PinnedArray<float>((size_t)p->n_views * p->isx * p->isy);
+        const int n = p->n_views;
+        const int T = std::max(1, std::min<int>(n, (int)std::thread::hardware_concurrency()));
+        std::vector<std::thread> th;
+        for (int t = 0; t < T; ++t)
+            th.emplace_back([&, t] {
+                for (int k = t; k < n; k += T)
+                    bph::forward_project(ph, st->s.mats[(size_t)k], p->isx, p->isy, st->s.image(k));
+            });
+        for (auto& x : th) x.join();
+        *out = st.release();
+    });
+}
+
+int bp_stack_read(const char* path, bp_stack** out) {
+    if (!path || !out) return fail(BP_EINVAL, "null argument");
+    return guarded([&] { *out = new bp_stack{bph::read_stack(path)}; });
+}
+
+int bp_stack_write(const bp_stack* s, const char* path) {
+    if (!s || !path) return fail(BP_EINVAL, "null argument");
+    return guarded([&] { bph::write_stack(path, s->s); });
+}
+
+void bp_stack_dims(const bp_stack* s, uint32_t* isx, uint32_t* isy, uint32_t* count) {
+    if (!s) return;
+    if (isx) *isx = (uint32_t)s->s.isx;
+    if (isy) *isy = (uint32_t)s->s.isy;
+    if (count) *count = (uint32_t)s->s.count();
+}
+
+void bp_stack_free(bp_stack* s) { delete s; }
+
+int bp_stack_create(uint32_t isx, uint32_t isy, uint32_t count, const double* matrices,
+                    const float* pixels, bp_stack** out) {
+    if (!out) return fail(BP_EINVAL, "null argument");
+    return guarded([&] {
+        if (isx < 2 || isy < 2) throw bph::config_error("detector must be at least 2x2 pixels");
+        if (count < 1) throw bph::config_error("need at least one view");
+        auto st = std::make_unique<bp_stack>();
+        st->s.isx = (int)isx;
+        st->s.isy = (int)isy;
+        st->s.mats.resize(count);
+        if (matrices)
+            for (uint32_t k = 0; k < count; ++k)
+                std::memcpy(st->s.mats[k].data(), matrices + 12 * (size_t)k, 12 * sizeof(double));
+        st->s.pixels = bph::PinnedArray<float>((size_t)count * isx * isy);
+        if (pixels)
+            std::memcpy(st->s.pixels.data(), pixels, (size_t)count * isx * isy * sizeof(float));
+        else
+            std::memset(st->s.pixels.data(), 0, (size_t)count * isx * isy * sizeof(float));
+        *out = st.release();
+    });
+}
+
+float* bp_stack_pixels(bp_stack* s) { return s ? s->s.pixels.data() : nullptr; }
+double* bp_stack_matrices(bp_stack* s) {
+    return s && !s->s.mats.empty() ? s->s.mats[0].data() : nullptr;
+}
+
+void bp_baseline_params_init(bp_baseline_params* p) {
+    if (!p) return;
+    bph::BaselineSpec d;
+    p->seed = d.seed;
+    p->n_views = d.n_views;
+    p->isx = d.isx;
+    p->isy = d.isy;
+    p->sid_mm = d.sid;
+    p->sdd_mm = d.sdd;
+    p->pitch_mm = d.pitch;
+    p->arc_deg = d.arc_deg;
+    p->jitter_mm = d.jitter_mm;
+    p->jitter_deg = d.jitter_deg;
+    p->n_ellipsoids = d.n_ellipsoids;
+    p->filter = d.filter;
+    p->threads = d.threads;
+}
+
+static bph::BaselineSpec spec_of(const bp_baseline_params* p) {
+    bph::BaselineSpec s;
+    s.seed = p->seed;
+    s.n_views = p->n_views;
+    s.isx = p->isx;
+    s.isy = p->isy;
+    s.sid = p->sid_mm;
+    s.sdd = p->sdd_mm;
+    s.pitch = p->pitch_mm;
+    s.arc_deg = p->arc_deg;
+    s.jitter_mm = p->jitter_mm;
+    s.jitter_deg = p->jitter_deg;
+    s.n_ellipsoids = p->n_ellipsoids;
+    s.filter = p->filter;
+    s.threads = p->threads;
+    return s;
+}
+
+int bp_stack_generate_baseline(const bp_baseline_params* p, bp_stack** out) {
+    if (!p || !out) return fail(BP_EINVAL, "null argument");
+    return guarded([&] { *out = new bp_stack{bph::make_baseline_stack(spec_of(p))}; });
+}
+
+int bp_baseline_phantom(const bp_baseline_params* p, double* ell, int max_n, int* n) {
+    if (!p || !n) return fail(BP_EINVAL, "null argument");
+    return guarded([&] {
+        const auto e = bph::baseline_phantom(spec_of(p));
+        *n = (int)e.size();
+        for (int i = 0; i < std::min<int>(max_n, (int)e.size()); ++i) {
+            const auto& x = e[(size_t)i];
+            const double v[7] = {x.cx, x.cy, x.cz, x.ax, x.ay, x.az, x.density};
+            std::memcpy(ell + 7 * i, v, sizeof v);
+        }
+    });
+}
+
+// ---- volumes --------------------------------------------------------------
+
+int bp_volume_read(const char* path, bp_volume** out) {
+    if (!path || !out) return fail(BP_EINVAL, "null argument");
+    return guarded([&] { *out = new bp_volume{bph::read_volume(path)}; });
+}
+
+int bp_volume_write(const bp_volume* v, const char* path) {
+    if (!v || !path) return fail(BP_EINVAL, "null argument");
+    return guarded([&] { bph::write_volume(path, v->v); });
+}
+
+uint32_t bp_volume_edge(const bp_volume* v) { return v ? (uint32_t)v->v.grid.L : 0; }
+const float* bp_volume_data(const bp_volume* v) { return v ? v->v.vox.data() : nullptr; }
+float* bp_volume_data_mut(bp_volume* v) { return v ? v->v.vox.data() : nullptr; }
+void bp_volume_free(bp_volume* v) { delete v; }
+
+int bp_volume_create(uint32_t l, bp_volume** out) {
+    if (!out) return fail(BP_EINVAL, "null argument");
+    return guarded([&] {
+        auto v = std::make_unique<bp_volume>(bp_volume{bph::Volume(bph::Grid::cube((int)l))});
+        std::memset(v->v.vox.data(), 0, v->v.vox.size() * sizeof(float));
+        *out = v.release();
+    });
+}
+
+int bp_psnr(const bp_volume* vol, const bp_volume* ref, double peak, double* out_db) {
+    if (!vol || !ref || !out_db) return fail(BP_EINVAL, "null argument");
+    return guarded([&] {
+        if (vol->v.grid.L != ref->v.grid.L) throw bph::validation_error("volume dimensions differ");
+        *out_db = bph::psnr(vol->v.vox.data(), ref->v.vox.data(), vol->v.vox.size(), peak);
+    });
+}
+
+// ---- streaming module ABI -----------------------------------------------------
+
+void bp_gpu_config_init(bp_gpu_config* c) {
+    if (!c) return;
+    std::memset(c, 0, sizeof *c);
+    c->device = -1;
+    c->view_batch = 32;
+    c->ring_batches = 3;
+    c->strict_mode = 1;
+    c->distance_weight = 1;
+    c->row_windows = 1;
+}
+
+int bp_gpu_load(const bp_gpu_config* cfg, bp_gpu_ctx** out) {
+    if (!cfg || !out) return fail(BP_EINVAL, "null argument");
+    return guarded([&] {
+        if (cfg->recip_mode < BP_RECIP_EXACT || cfg->recip_mode > BP_RECIP_APPROX12_NR)
+            throw bph::config_error("recip_mode out of range");
+        auto c = std::make_unique<bp_gpu_ctx>();
+        c->c = std::make_unique<bpr::SlabContext>(*cfg);
+        *out = c.release();
+    });
+}
+
+int bp_gpu_backproject(bp_gpu_ctx* ctx, const float* image, const double matrix[12]) {
+    if (!ctx || !image || !matrix) return fail(BP_EINVAL, "null argument");
+    return guarded([&] { ctx->c->backproject(image, matrix, true); });
+}
+
+int bp_gpu_backproject_async(bp_gpu_ctx* ctx, const float* image, const double matrix[12]) {
+    if (!ctx || !image || !matrix) return fail(BP_EINVAL, "null argument");
+    return guarded([&] { ctx->c->backproject(image, matrix, false); });
+}
+
+int bp_gpu_finish(bp_gpu_ctx* ctx, float* host_volume, bp_gpu_stats* stats) {
+    if (!ctx) return fail(BP_EINVAL, "null argument");
+    return guarded([&] { ctx->c->finish(host_volume, stats); });
+}
+
+int bp_gpu_unload(bp_gpu_ctx* ctx) {
+    if (!ctx) return fail(BP_EINVAL, "null argument");
+    return guarded([&] { delete ctx; });
+}
+
+int bp_gpu_volume_device(bp_gpu_ctx* ctx, float** dptr, int* z_begin, int* z_end) {
+    if (!ctx) return fail(BP_EINVAL, "null argument");
+    if (dptr) *dptr = ctx->c->device_volume();
+    if (z_begin) *z_begin = ctx->c->z_begin();
+    if (z_end) *z_end = ctx->c->z_end();
+    return BP_OK;
+}
+
+int bp_gpu_upload_views(bp_gpu_ctx* ctx, const float* pixels, const double* matrices, int count) {
+    if (!ctx || !pixels || !matrices) return fail(BP_EINVAL, "null argument");
+    return guarded([&] { ctx->c->upload_views(pixels, matrices, count); });
+}
+
+int bp_gpu_time_resident(bp_gpu_ctx* ctx, int iters, double* device_ms, bp_gpu_stats* stats) {
+    if (!ctx) return fail(BP_EINVAL, "null argument");
+    return guarded([&] {
+        const double ms = ctx->c->time_resident(iters, stats);
+        if (device_ms) *device_ms = ms;
+    });
+}
+
+// ---- multi-GPU / partition -----------------------------------------------------
+
+int bp_gpu_set_devices(const int* devices, int n) {
+    if (!devices || n < 1) return fail(BP_EINVAL, "need at least one device");
+    std::lock_guard<std::mutex> g(g_dev_mu);
+    g_devices.assign(devices, devices + n);
+    return BP_OK;
+}
+
+int bp_gpu_device_count(int* n) {
+    if (!n) return fail(BP_EINVAL, "null argument");
+    int c = 0;
+    if (cudaGetDeviceCount(&c) != cudaSuccess) {
+        cudaGetLastError();
+        c = 0;
+    }
+    *n = c;
+    return BP_OK;
+}
+
+int bp_partition_slabs(const double* matrices, int count, uint32_t isx, uint32_t isy, uint32_t l,
+                       const double offset_mm[3], int G, int* bounds) {
+    if (!matrices || !bounds || count < 1) return fail(BP_EINVAL, "null argument");
+    return guarded([&] {
+        std::vector<bph::Mat> m((size_t)count);
+        for (int k = 0; k < count; ++k) std::memcpy(m[(size_t)k].data(), matrices + 12 * k, 96);
+        const double* o = offset_mm;
+        auto g = bph::Grid::cube((int)l, o ? o[0] : 0, o ? o[1] : 0, o ? o[2] : 0);
+        auto b = bph::partition_slabs(m, (int)isx, (int)isy, g, G);
+        std::copy(b.begin(), b.end(), bounds);
+    });
+}
+
+int bp_slab_row_window(const double matrix[12], uint32_t isy, uint32_t l, const double offset_mm[3],
+                       int z_begin, int z_end, int* r0, int* r1) {
+    if (!matrix || !r0 || !r1) return fail(BP_EINVAL, "null argument");
+    return guarded([&] {
+        const double* o = offset_mm;
+        auto g = bph::Grid::cube((int)l, o ? o[0] : 0, o ? o[1] : 0, o ? o[2] : 0);
+        if (z_begin < 0 || z_end > (int)l || z_begin >= z_end)
+            throw bph::config_error("slab out of range");
+        bph::Mat m;
+        std::memcpy(m.data(), matrix, 96);
+        bph::row_window(m, g, 0, (int)l - 1, 0, (int)l - 1, z_begin, z_end - 1, (int)isy, r0, r1);
+    });
+}
+
+void bp_recon_ex_init(bp_recon_ex* p) {
+    if (!p) return;
+    std::memset(p, 0, sizeof *p);
+    p->view_batch = 32;
+    p->strict_mode = 1;
+    p->distance_weight = 1;
+    p->row_windows = 1;
+}
+
+int bp_reconstruct_ex(const bp_stack* s, uint32_t l, const bp_recon_ex* p, float* host_volume,
+                      bp_gpu_stats* stats) {
+    if (!s || !p || !host_volume) return fail(BP_EINVAL, "null argument");
+    return guarded([&] {
+        if (l < 1) throw bph::config_error("grid edge must be >= 1 voxel");
+        if (s->s.count() < 1) throw bph::validation_error("empty projection stack");
+        std::vector<int> devs;
+        {
+            std::lock_guard<std::mutex> g(g_dev_mu);
+            devs = g_devices;
+        }
+        if (p->n_devices > 0) devs.resize(std::min<size_t>(devs.size(), (size_t)p->n_devices));
+        if (p->n_devices > (int)devs.size())
+            for (int d = (int)devs.size(); d < p->n_devices; ++d) devs.push_back(d);
+        const int D = (int)devs.size();
+        const int G = std::max(D, p->virtual_slabs);
+        const double off[3] = {p->offset_mm ? p->offset_mm[0] : 0.0,
+                               p->offset_mm ? p->offset_mm[1] : 0.0,
+                               p->offset_mm ? p->offset_mm[2] : 0.0};
+        const auto grid = bph::Grid::cube((int)l, off[0], off[1], off[2]);
+        // reference: every matrix is validated before any work (scheduler.cpp:35)
+        for (const auto& m : s->s.mats) bph::validate_matrix_for_grid(m, grid);
+        std::vector<int> bounds = {0, (int)l};
+        if (G > 1) bounds = bph::partition_slabs(s->s.mats, s->s.isx, s->s.isy, grid, G);
+        std::vector<bp_gpu_stats> per((size_t)G);
+        std::vector<std::string> errs((size_t)D);
+        std::vector<int> codes((size_t)D, BP_OK);
+        auto worker = [&](int d) {
+            codes[(size_t)d] = guarded([&] {
+                for (int g = d; g < G; g += D) {
+                    bp_gpu_config c;
+                    bp_gpu_config_init(&c);
+                    c.l = l;
+                    c.isx = (uint32_t)s->s.isx;
+                    c.isy = (uint32_t)s->s.isy;
+                    std::memcpy(c.offset_mm, off, sizeof off);
+                    c.device = devs[(size_t)d];
+                    c.z_begin = bounds[(size_t)g];
+                    c.z_end = bounds[(size_t)g + 1];
+                    c.view_batch = p->view_batch > 0 ? p->view_batch : 32;
+                    c.strict_mode = p->strict_mode;
+                    c.distance_weight = p->distance_weight;
+                    c.row_windows = p->row_windows;
+                    c.kernel = p->kernel;
+                    c.count_visible = p->count_visible;
+                    c.recip_mode = p->recip_mode;
+                    auto ctx = acquire(c);
+                    for (int k = 0; k < s->s.count(); ++k)
+                        ctx->backproject(s->s.image(k), s->s.mats[(size_t)k].data(), false);
+                    ctx->finish(host_volume + (size_t)c.z_begin * l * l, &per[(size_t)g]);
+                    release(std::move(ctx));
+                }
+            });
+            if (codes[(size_t)d] != BP_OK) errs[(size_t)d] = g_last_error;
+        };
+        if (D == 1) {
+            worker(0);
+        } else {
+            std::vector<std::thread> th;
+            for (int d = 0; d < D; ++d) th.emplace_back(worker, d);
+            for (auto& t : th) t.join();
+        }
+        for (int d = 0; d < D; ++d)
+            if (codes[(size_t)d] != BP_OK) {
+                const int c = codes[(size_t)d];
+                const std::string m = "device " + std::to_string(devs[(size_t)d]) + ": " + errs[(size_t)d];
+                if (c == BP_EINVAL) throw bph::config_error(m);
+                if (c == BP_EVERIFY) throw bph::validation_error(m);
+                if (c == BP_EIO) throw bph::io_error(m);
+                throw bph::device_error(m);
+            }
+        if (stats) {
+            bp_gpu_stats t{};
+            for (const auto& x : per) {
+                t.wall_ms = std::max(t.wall_ms, x.wall_ms);
+                t.device_ms = std::max(t.device_ms, x.device_ms);
+                t.kernel_ms += x.kernel_ms;
+                t.h2d_ms = std::max(t.h2d_ms, x.h2d_ms);
+                t.d2h_ms = std::max(t.d2h_ms, x.d2h_ms);
+                t.views = x.views;
+                t.launches += x.launches;
+                t.nominal_updates += x.nominal_updates;
+                t.visible_updates += x.visible_updates;
+                t.tile_pairs += x.tile_pairs;
+                t.skipped_pairs += x.skipped_pairs;
+                t.fallback_pairs += x.fallback_pairs;
+                t.h2d_bytes += x.h2d_bytes;
+                t.d2h_bytes += x.d2h_bytes;
+                t.tile_w = std::max(t.tile_w, x.tile_w);
+                t.tile_h = std::max(t.tile_h, x.tile_h);
+                t.block_x = x.block_x;
+                t.block_y = x.block_y;
+                t.block_z = x.block_z;
+            }
+            *stats = t;
+        }
+    });
+}
+
+// ---- reference one-shot entry point ------------------------------------------------
+
+int bp_reconstruct(const bp_stack* s, const bp_recon_params* p, bp_volume** out,
+                   bp_recon_stats* stats) {
+    if (!s || !p || !out) return fail(BP_EINVAL, "null argument");
+    return guarded([&] {
+        // parameter mapping and validation of capi.cpp:113-130 / scheduler.cpp:31-34
+        if (p->recip_mode < BP_RECIP_EXACT || p->recip_mode > BP_RECIP_APPROX12_NR)
+            throw bph::config_error("recip_mode out of range");
+        if (p->extract != BP_EXTRACT_V1_STORE && p->extract != BP_EXTRACT_V2_SHIFT)
+            throw bph::config_error("extract out of range");
+        const int threads = p->threads;
+        const int chunk = p->chunk > 0 ? p->chunk : 1;
+        const int block_b = p->block_b > 0 ? p->block_b : 32;
+        const int lanes = p->lanes > 0 ? p->lanes : 1;
+        const int numa = p->numa_domains > 0 ? p->numa_domains : 1;
+        auto grid = bph::Grid::cube((int)p->l);
+        if (s->s.count() < 1) throw bph::validation_error("empty projection stack");
+        if (threads < 1 || chunk < 1 || block_b < 1 || numa < 1)
+            throw bph::config_error("threads, chunk, block_b and numa_domains must be >= 1");
+        if (lanes != 1 && lanes != 4 && lanes != 8)
+            throw bph::config_error("lane width must be 1, 4 or 8");
+        if (block_b > 64) throw bph::config_error("block_b (view batch) must be <= 64 on the GPU");
+
+        auto vol = std::make_unique<bp_volume>(bp_volume{bph::Volume(grid)});
+        bp_recon_ex ex;
+        bp_recon_ex_init(&ex);
+        ex.view_batch = block_b;
+        ex.strict_mode = p->strict_mode != 0 ? 1 : 0;
+        ex.distance_weight = p->distance_weight != 0 ? 1 : 0;
+        ex.count_visible = p->clip != 0 ? 1 : 0;
+        ex.recip_mode = p->recip_mode;
+        bp_gpu_stats gs{};
+        const double t0 = bpr::now_ms();
+        const int rc = bp_reconstruct_ex(s, p->l, &ex, vol->v.vox.data(), &gs);
+        if (rc != BP_OK) {
+            const std::string m = g_last_error;
+            if (rc == BP_EINVAL) throw bph::config_error(m);
+            if (rc == BP_EVERIFY) throw bph::validation_error(m);
+            if (rc == BP_EIO) throw bph::io_error(m);
+            throw bph::device_error(m);
+        }
+        const double secs = (bpr::now_ms() - t0) / 1e3;
+        *out = vol.release();
+        if (stats) {
+            *stats = {};
+            const uint64_t L3 = (uint64_t)p->l * p->l * p->l;
+            const uint64_t n = (uint64_t)s->s.count();
+            stats->seconds = secs;
+            stats->voxel_updates = p->clip ? gs.visible_updates : n * L3;
+            stats->gups = secs > 0 ? stats->voxel_updates / secs / 1e9 : 0.0;
+            stats->gflops = secs > 0 ? 31.0 * stats->voxel_updates / secs / 1e9 : 0.0;
+            stats->writeback_stores = (n + block_b - 1) / block_b * L3;
+            stats->bytes_copied = gs.h2d_bytes;
+            stats->clip_reduction = p->clip ? 1.0 - (double)gs.visible_updates / (double)(n * L3) : 0.0;
+            stats->thread_updates_min = stats->voxel_updates;
+            stats->thread_updates_max = stats->voxel_updates;
+        }
+    });
+}
+
+int bp_selftest_rcp(uint32_t lo_bits, uint32_t hi_bits, uint64_t* mismatches) {
+    if (!mismatches) return fail(BP_EINVAL, "null argument");
+    return guarded([&] {
+        unsigned long long m = 0;
+        bpr::check((cudaError_t)bpg::selftest_rcp(lo_bits, hi_bits, &m), "rcp selftest");
+        *mismatches = m;
+    });
+}
+
+// ---- performance model: out of scope ------------------------------
+
+static const char* kModelOut =
+    "the analytic CPU performance model (proj/src/perfmodel.cpp) is out of scope of the B200 build";
+
+int bp_machine_load(const char*, bp_machine** out) {
+    if (out) *out = nullptr;
+    return fail(BP_EINVAL, kModelOut);
+}
+void bp_machine_free(bp_machine* m) { delete m; }
+int bp_model_report_build(const bp_machine*, bp_model_report*) { return fail(BP_EINVAL, kModelOut); }
+int bp_machine_measure(bp_machine*, size_t, int, double) { return fail(BP_EINVAL, kModelOut); }
+int bp_model_deviation(const bp_machine*, double, double*) { return fail(BP_EINVAL, kModelOut); }
+
+}  // extern "C"

@@ -1,0 +1,80 @@
+// bp_device.hpp -- host/device shared launch structures for the backprojection
+// kernels (bp_kernels.cu) and the host pipeline (bp_runtime.cpp).
+//
+// Reference path replaced: bp::reconstruct's blocked view loop
+// (proj/src/scheduler.cpp:77-100) driving bp::line_update_scalar
+// (proj/src/kernel.cpp:49-85).  One kernel launch here = one "projection block"
+// of the reference (block_b views), with the voxel accumulators held in
+// registers across the batch instead of the reference's per-line linebuf.
+#pragma once
+
+#include <cstdint>
+
+namespace bpg {
+
+// Maximum views per kernel launch (register batch).  The per-view matrices
+// travel as kernel parameters (constant bank), so the batch is bounded by the
+// 32 KB parameter space; 64 x 48 B + extras stays far below it.
+constexpr int kMaxBatch = 64;
+
+// One launch = one batch of views against one z-slab of the volume.
+struct BatchArgs {
+    int nviews;                  // views in this batch (1..kMaxBatch)
+    int load_volume;             // 0: first batch, accumulators start at +0
+    int slot[kMaxBatch];         // projection slot (ring index) of view k
+    float A[kMaxBatch][12];      // narrowed matrices, reference a[] layout (geometry.hpp:25-37)
+};
+
+struct SlabArgs {
+    float* vol;                  // slab volume [nz][L][L], x fastest (kernel.hpp:26-33)
+    const float* proj;           // projection ring [slots][isy][pitch]
+    const float* wx;             // world x of voxel i, float(offset_x + i*MM) (kernel.cpp:62)
+    const float* wy;
+    const float* wz;             // indexed by GLOBAL z
+    unsigned long long* counters;  // [0]=tile pairs [1]=skipped pairs [2]=fallback pairs
+    int L;                       // voxels per edge
+    int z0;                      // first global z of the slab
+    int nz;                      // slab depth
+    int isx, isy;                // detector size
+    int pitch;                   // row pitch of a projection slot, floats (multiple of 4)
+    int nbx, nby, nbz;           // voxel blocks of the tiled kernel
+};
+
+// Launchers (bp_kernels.cu).  All asynchronous on `stream`.
+enum KernelKind : int { kKernelAuto = 0, kKernelSimple = 1 };
+
+struct TileShape {
+    int bx, by, bz;              // voxel block
+    int tw, th;                  // tile capacity (floats), tw % 4 == 0, th % 8 == 0
+    int stages;
+    int threads;                 // consumer + producer threads per CTA
+    int smem_bytes;
+};
+
+// Picks the tiled-kernel variant for edge length L (returns false if the
+// tiled kernel cannot serve this L, e.g. odd L).
+bool tile_shape_for(int L, TileShape* out);
+
+// Encodes the TMA descriptor over the projection ring (CUtensorMap, 128 B).
+// Returns 0 on success.
+int encode_ring_tmap(void* tmap128, const float* ring, int isx, int isy, int pitch, int slots,
+                     const TileShape& ts, char* err, int errlen);
+
+int launch_tiled(const void* tmap128, const SlabArgs& s, const BatchArgs& b,
+                 const TileShape& ts, bool strict, bool distance_weight, void* stream);
+
+// recip: 0 exact (recip.hpp:12), 1 approx12 (recip.hpp:14-18), 2 approx12_nr (recip.hpp:20-23)
+int launch_simple(const SlabArgs& s, const BatchArgs& b, bool distance_weight, int recip,
+                  void* stream);
+
+int smem_bytes_for(const TileShape& ts);
+
+// Bitwise check of the kernel's paired reciprocal against __frcp_rn over the
+// float bit patterns [lo_bits, hi_bits).  Synchronous.
+int selftest_rcp(uint32_t lo_bits, uint32_t hi_bits, unsigned long long* mismatches);
+
+// Exact visible-update count (clip_stats semantics, precompute.cpp:93-103)
+// for views [0,n) of the batch: adds into counters[3].
+int launch_clip_count(const SlabArgs& s, const BatchArgs& b, void* stream);
+
+}  // namespace bpg

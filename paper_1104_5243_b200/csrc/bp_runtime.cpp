@@ -1,0 +1,456 @@
+// bp_runtime.cpp -- see bp_runtime.hpp.
+#include "bp_runtime.hpp"
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <string>
+
+namespace bpr {
+
+void check(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        throw bph::device_error(std::string(what) + ": " + cudaGetErrorString(e));
+    }
+}
+
+double now_ms() {
+    return std::chrono::duration<double, std::milli>(
+               std::chrono::steady_clock::now().time_since_epoch())
+        .count();
+}
+
+namespace {
+int round_up(int v, int m) { return (v + m - 1) / m * m; }
+}  // namespace
+
+void SlabContext::bind() const { check(cudaSetDevice(dev_), "cudaSetDevice"); }
+
+SlabContext::SlabContext(const bp_gpu_config& cfg) : cfg_(cfg) {
+    if (cfg.l < 1) throw bph::config_error("grid edge must be >= 1 voxel");
+    if (cfg.isx < 2 || cfg.isy < 2) throw bph::config_error("detector must be at least 2x2 pixels");
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev < 1) {
+        cudaGetLastError();
+        throw bph::device_error("no CUDA device available (the GPU path has no CPU fallback)");
+    }
+    if (cfg.device >= 0) {
+        if (cfg.device >= ndev) throw bph::config_error("device ordinal out of range");
+        dev_ = cfg.device;
+    } else {
+        check(cudaGetDevice(&dev_), "cudaGetDevice");
+    }
+    bind();
+    L_ = (int)cfg.l;
+    grid_ = bph::Grid::cube(L_, cfg.offset_mm[0], cfg.offset_mm[1], cfg.offset_mm[2]);
+    z0_ = cfg.z_begin;
+    z1_ = cfg.z_end > 0 ? cfg.z_end : L_;
+    if (z0_ < 0 || z1_ > L_ || z0_ >= z1_) throw bph::config_error("slab [z_begin, z_end) out of range");
+    nz_ = z1_ - z0_;
+    isx_ = (int)cfg.isx;
+    isy_ = (int)cfg.isy;
+    pitch_ = round_up(isx_, 4);  // TMA global strides must be multiples of 16 B
+    B_ = cfg.view_batch > 0 ? cfg.view_batch : 32;
+    if (B_ > bpg::kMaxBatch) throw bph::config_error("view_batch exceeds 64");
+    R_ = cfg.ring_batches > 0 ? cfg.ring_batches : 3;
+    slots_ = B_ * R_;
+
+    const size_t vol_elems = (size_t)nz_ * L_ * L_;
+    if (cfg.device_volume) {
+        own_vol_ = false;
+        d_vol_ = cfg.device_volume;
+    } else {
+        check(cudaMalloc(&d_vol_, vol_elems * sizeof(float)), "cudaMalloc(volume)");
+    }
+    check(cudaMalloc(&d_ring_, (size_t)slots_ * isy_ * pitch_ * sizeof(float)), "cudaMalloc(ring)");
+    check(cudaMemset(d_ring_, 0, (size_t)slots_ * isy_ * pitch_ * sizeof(float)), "cudaMemset(ring)");
+    const int tab = L_ + 160;  // padded so nominal block extents beyond L stay in-table
+    auto hwx = bph::world_table(grid_.ox, grid_.MM, tab);
+    auto hwy = bph::world_table(grid_.oy, grid_.MM, tab);
+    auto hwz = bph::world_table(grid_.oz, grid_.MM, tab);
+    check(cudaMalloc(&d_wx_, tab * sizeof(float)), "cudaMalloc(tables)");
+    check(cudaMalloc(&d_wy_, tab * sizeof(float)), "cudaMalloc(tables)");
+    check(cudaMalloc(&d_wz_, tab * sizeof(float)), "cudaMalloc(tables)");
+    check(cudaMemcpy(d_wx_, hwx.data(), tab * sizeof(float), cudaMemcpyHostToDevice), "tables");
+    check(cudaMemcpy(d_wy_, hwy.data(), tab * sizeof(float), cudaMemcpyHostToDevice), "tables");
+    check(cudaMemcpy(d_wz_, hwz.data(), tab * sizeof(float), cudaMemcpyHostToDevice), "tables");
+    check(cudaMalloc(&d_cnt_, 8 * sizeof(unsigned long long)), "cudaMalloc(counters)");
+    check(cudaMemset(d_cnt_, 0, 8 * sizeof(unsigned long long)), "cudaMemset(counters)");
+    check(cudaStreamCreateWithFlags(&s_comp_, cudaStreamNonBlocking), "stream");
+    check(cudaStreamCreateWithFlags(&s_copy_, cudaStreamNonBlocking), "stream");
+    ev_ready_.resize((size_t)R_);
+    ev_free_.resize((size_t)R_);
+    used_.assign((size_t)R_, false);
+    for (int i = 0; i < R_; ++i) {
+        check(cudaEventCreateWithFlags(&ev_ready_[(size_t)i], cudaEventDisableTiming), "event");
+        check(cudaEventCreateWithFlags(&ev_free_[(size_t)i], cudaEventDisableTiming), "event");
+    }
+    for (cudaEvent_t* e : {&ev_t0_, &ev_t1_, &ev_h0_, &ev_h1_, &ev_d0_, &ev_d1_})
+        check(cudaEventCreate(e), "event");
+    std::memset(tmap_, 0, sizeof tmap_);
+    reset_recon();
+}
+
+SlabContext::~SlabContext() {
+    cudaSetDevice(dev_);
+    if (s_comp_) cudaStreamSynchronize(s_comp_);
+    if (s_copy_) cudaStreamSynchronize(s_copy_);
+    for (auto e : ev_ready_) cudaEventDestroy(e);
+    for (auto e : ev_free_) cudaEventDestroy(e);
+    for (auto& p : launch_ev_) {
+        cudaEventDestroy(p.first);
+        cudaEventDestroy(p.second);
+    }
+    for (cudaEvent_t e : {ev_t0_, ev_t1_, ev_h0_, ev_h1_, ev_d0_, ev_d1_})
+        if (e) cudaEventDestroy(e);
+    if (s_comp_) cudaStreamDestroy(s_comp_);
+    if (s_copy_) cudaStreamDestroy(s_copy_);
+    if (own_vol_ && d_vol_) cudaFree(d_vol_);
+    cudaFree(d_ring_);
+    cudaFree(d_wx_);
+    cudaFree(d_wy_);
+    cudaFree(d_wz_);
+    cudaFree(d_cnt_);
+    if (h_stage_) bph::pinned_free(h_stage_);
+    cudaGetLastError();
+}
+
+void SlabContext::reset_recon() {
+    nb_ = 0;
+    any_launch_ = false;
+    any_h2d_ = false;
+    views_ = 0;
+    launches_ = 0;
+    h2d_bytes_ = 0;
+    launch_ev_used_ = 0;
+    wall_t0_ = 0.0;
+}
+
+void SlabContext::backproject(const float* image, const double* A, bool copy) {
+    if (!image || !A) throw bph::config_error("null argument");
+    bind();
+    if (resident_ > 0) resident_ = 0;  // streaming reuses the slots
+    if (views_ == 0) wall_t0_ = now_ms();
+    bph::Mat m;
+    std::memcpy(m.data(), A, sizeof(double) * 12);
+    bph::validate_matrix_for_grid(m, grid_);
+
+    if (nb_ == 0 && used_[(size_t)rg_]) {
+        // the ring group (and its pinned staging) is reusable once the kernel
+        // that last read it has finished
+        check(cudaEventSynchronize(ev_free_[(size_t)rg_]), "ring wait");
+    }
+    int r0 = 0, r1 = isy_;
+    if (cfg_.row_windows)
+        bph::row_window(m, grid_, 0, L_ - 1, 0, L_ - 1, z0_, z1_ - 1, isy_, &r0, &r1);
+    const int slot = rg_ * B_ + nb_;
+    if (r1 > r0) {
+        const float* src = image + (size_t)r0 * isx_;
+        if (copy) {
+            if (!h_stage_)
+                h_stage_ = static_cast<float*>(
+                    bph::pinned_alloc((size_t)slots_ * isy_ * isx_ * sizeof(float)));
+            float* stg = h_stage_ + (size_t)slot * isy_ * isx_ + (size_t)r0 * isx_;
+            std::memcpy(stg, src, (size_t)(r1 - r0) * isx_ * sizeof(float));
+            src = stg;
+        }
+        if (!any_h2d_) {
+            check(cudaEventRecord(ev_h0_, s_copy_), "event");
+            any_h2d_ = true;
+        }
+        float* dst = d_ring_ + (size_t)slot * isy_ * pitch_ + (size_t)r0 * pitch_;
+        if (pitch_ == isx_)
+            check(cudaMemcpyAsync(dst, src, (size_t)(r1 - r0) * isx_ * sizeof(float),
+                                  cudaMemcpyHostToDevice, s_copy_),
+                  "H2D");
+        else
+            check(cudaMemcpy2DAsync(dst, (size_t)pitch_ * sizeof(float), src,
+                                    (size_t)isx_ * sizeof(float), (size_t)isx_ * sizeof(float),
+                                    (size_t)(r1 - r0), cudaMemcpyHostToDevice, s_copy_),
+                  "H2D");
+        h2d_bytes_ += (uint64_t)(r1 - r0) * isx_ * sizeof(float);
+    }
+    const auto f = bph::narrowed(m);
+    std::memcpy(cur_.A[nb_], f.data(), sizeof(float) * 12);
+    cur_.slot[nb_] = slot;
+    ++nb_;
+    ++views_;
+    if (nb_ == B_) flush();
+}
+
+void SlabContext::choose_tile(const bpg::BatchArgs& b) {
+    if (cfg_.kernel == bpg::kKernelSimple || cfg_.recip_mode != 0) {
+        tiled_ = false;
+        return;
+    }
+    bpg::TileShape t{};
+    if (!bpg::tile_shape_for(L_, &t)) {
+        tiled_ = false;
+        return;
+    }
+    // Sample the block lattice (including the outermost blocks, whose shadows
+    // are the largest) for a few views of this batch; size the SMEM tile from
+    // the largest footprint plus a guard.  Pairs that still do not fit are
+    // served exactly by the in-kernel global-memory fallback.
+    const int nbx = (L_ + t.bx - 1) / t.bx, nby = (L_ + t.by - 1) / t.by,
+              nbz = (nz_ + t.bz - 1) / t.bz;
+    auto samples = [](int n) {
+        std::vector<int> s;
+        const int k = std::min(n, 9);
+        for (int i = 0; i < k; ++i) s.push_back(k == 1 ? 0 : (int)((long long)i * (n - 1) / (k - 1)));
+        return s;
+    };
+    const auto sx = samples(nbx), sy = samples(nby), sz = samples(nbz);
+    const int views[3] = {0, b.nviews / 2, b.nviews - 1};
+    int need_w = 0, need_h = 0;
+    for (int vi = 0; vi < 3; ++vi) {
+        const float* A = b.A[views[vi]];
+        for (int zi : sz)
+            for (int yi : sy)
+                for (int xi : sx) {
+                    double umin = 1e300, umax = -1e300, vmin = 1e300, vmax = -1e300, wmin = 1e300;
+                    for (int c = 0; c < 8; ++c) {
+                        const int x = xi * t.bx + ((c & 1) ? t.bx - 1 : 0);
+                        const int y = yi * t.by + ((c & 2) ? t.by - 1 : 0);
+                        const int z = z0_ + zi * t.bz + ((c & 4) ? t.bz - 1 : 0);
+                        const double wx = (double)(float)grid_.wx(x), wy = (double)(float)grid_.wy(y),
+                                     wz = (double)(float)grid_.wz(z);
+                        const double uw = (double)A[0] * wx + (double)A[3] * wy + (double)A[6] * wz + (double)A[9];
+                        const double vw = (double)A[1] * wx + (double)A[4] * wy + (double)A[7] * wz + (double)A[10];
+                        const double w = (double)A[2] * wx + (double)A[5] * wy + (double)A[8] * wz + (double)A[11];
+                        wmin = std::min(wmin, w);
+                        umin = std::min(umin, uw / w);
+                        umax = std::max(umax, uw / w);
+                        vmin = std::min(vmin, vw / w);
+                        vmax = std::max(vmax, vw / w);
+                    }
+                    if (!(wmin > 0) || std::fabs(umin) > 1e6 || std::fabs(umax) > 1e6 ||
+                        std::fabs(vmin) > 1e6 || std::fabs(vmax) > 1e6)
+                        continue;
+                    const int iu0 = (int)std::floor(umin) - 1, iu1 = (int)std::floor(umax) + 2;
+                    const int iv0 = (int)std::floor(vmin) - 1, iv1 = (int)std::floor(vmax) + 2;
+                    if (iu1 < 0 || iu0 > isx_ - 1 || iv1 < 0 || iv0 > isy_ - 1) continue;
+                    need_w = std::max(need_w, iu1 - iu0 + 1);
+                    need_h = std::max(need_h, iv1 - iv0 + 1);
+                }
+    }
+    int tw = round_up(std::max(need_w, 8) + 8, 4);
+    int th = round_up(std::max(need_h, 8) + 8, 8);
+    tw = std::min(tw, 256);
+    th = std::min(th, 256);
+    if (tiled_ && tw <= ts_.tw && th <= ts_.th) return;
+    if (tiled_) {
+        tw = std::max(tw, ts_.tw);
+        th = std::max(th, ts_.th);
+    }
+    // keep the CTA's dynamic shared memory within the SM budget
+    t.tw = tw;
+    t.th = th;
+    while (bpg::smem_bytes_for(t) > 220 * 1024 && t.th > 8) t.th -= 8;
+    t.smem_bytes = bpg::smem_bytes_for(t);
+    char err[256];
+    if (bpg::encode_ring_tmap(tmap_, d_ring_, isx_, isy_, pitch_, slots_, t, err, sizeof err) != 0)
+        throw bph::device_error(err);
+    ts_ = t;
+    tiled_ = true;
+}
+
+void SlabContext::launch(const bpg::BatchArgs& b) {
+    bpg::SlabArgs s{};
+    s.vol = d_vol_;
+    s.proj = d_ring_;
+    s.wx = d_wx_;
+    s.wy = d_wy_;
+    s.wz = d_wz_;
+    s.counters = d_cnt_;
+    s.L = L_;
+    s.z0 = z0_;
+    s.nz = nz_;
+    s.isx = isx_;
+    s.isy = isy_;
+    s.pitch = pitch_;
+    if (tiled_) {
+        s.nbx = (L_ + ts_.bx - 1) / ts_.bx;
+        s.nby = (L_ + ts_.by - 1) / ts_.by;
+        s.nbz = (nz_ + ts_.bz - 1) / ts_.bz;
+    }
+    if (cfg_.count_visible) check((cudaError_t)bpg::launch_clip_count(s, b, s_comp_), "clip count");
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (cfg_.profile_launches) {
+        if (launch_ev_used_ == launch_ev_.size()) {
+            cudaEvent_t a, c;
+            check(cudaEventCreate(&a), "event");
+            check(cudaEventCreate(&c), "event");
+            launch_ev_.emplace_back(a, c);
+        }
+        e0 = launch_ev_[launch_ev_used_].first;
+        e1 = launch_ev_[launch_ev_used_].second;
+        ++launch_ev_used_;
+        check(cudaEventRecord(e0, s_comp_), "event");
+    }
+    int rc;
+    if (tiled_)
+        rc = bpg::launch_tiled(tmap_, s, b, ts_, cfg_.strict_mode != 0, cfg_.distance_weight != 0,
+                               s_comp_);
+    else
+        rc = bpg::launch_simple(s, b, cfg_.distance_weight != 0, cfg_.recip_mode, s_comp_);
+    check((cudaError_t)rc, "backprojection kernel launch");
+    if (e1) check(cudaEventRecord(e1, s_comp_), "event");
+    ++launches_;
+}
+
+void SlabContext::flush() {
+    if (nb_ == 0) return;
+    cur_.nviews = nb_;
+    cur_.load_volume = any_launch_ ? 1 : 0;
+    choose_tile(cur_);
+    check(cudaEventRecord(ev_ready_[(size_t)rg_], s_copy_), "event");
+    check(cudaStreamWaitEvent(s_comp_, ev_ready_[(size_t)rg_], 0), "wait");
+    if (!any_launch_) check(cudaEventRecord(ev_t0_, s_comp_), "event");
+    launch(cur_);
+    any_launch_ = true;
+    check(cudaEventRecord(ev_free_[(size_t)rg_], s_comp_), "event");
+    used_[(size_t)rg_] = true;
+    rg_ = (rg_ + 1) % R_;
+    nb_ = 0;
+}
+
+void SlabContext::finish(float* host_volume, bp_gpu_stats* st) {
+    bind();
+    if (views_ == 0) wall_t0_ = now_ms();
+    flush();
+    if (!any_launch_) {
+        check(cudaEventRecord(ev_t0_, s_comp_), "event");
+        check(cudaMemsetAsync(d_vol_, 0, (size_t)nz_ * L_ * L_ * sizeof(float), s_comp_), "memset");
+    }
+    check(cudaEventRecord(ev_t1_, s_comp_), "event");
+    if (any_h2d_) check(cudaEventRecord(ev_h1_, s_copy_), "event");
+    const size_t vbytes = (size_t)nz_ * L_ * L_ * sizeof(float);
+    if (host_volume) {
+        check(cudaEventRecord(ev_d0_, s_comp_), "event");
+        check(cudaMemcpyAsync(host_volume, d_vol_, vbytes, cudaMemcpyDeviceToHost, s_comp_), "D2H");
+        check(cudaEventRecord(ev_d1_, s_comp_), "event");
+    }
+    unsigned long long cnt[8] = {0};
+    check(cudaMemcpyAsync(cnt, d_cnt_, sizeof cnt, cudaMemcpyDeviceToHost, s_comp_), "counters");
+    check(cudaMemsetAsync(d_cnt_, 0, sizeof cnt, s_comp_), "counters");
+    check(cudaStreamSynchronize(s_copy_), "sync");
+    check(cudaStreamSynchronize(s_comp_), "sync");
+    if (st) {
+        std::memset(st, 0, sizeof *st);
+        st->wall_ms = now_ms() - wall_t0_;
+        float ms = 0;
+        check(cudaEventElapsedTime(&ms, ev_t0_, ev_t1_), "elapsed");
+        st->device_ms = ms;
+        if (any_h2d_) {
+            check(cudaEventElapsedTime(&ms, ev_h0_, ev_h1_), "elapsed");
+            st->h2d_ms = ms;
+        }
+        if (host_volume) {
+            check(cudaEventElapsedTime(&ms, ev_d0_, ev_d1_), "elapsed");
+            st->d2h_ms = ms;
+            st->d2h_bytes = vbytes;
+        }
+        double kms = 0;
+        for (size_t i = 0; i < launch_ev_used_; ++i) {
+            check(cudaEventElapsedTime(&ms, launch_ev_[i].first, launch_ev_[i].second), "elapsed");
+            kms += ms;
+        }
+        st->kernel_ms = kms;
+        st->views = views_;
+        st->launches = launches_;
+        st->nominal_updates = views_ * (uint64_t)nz_ * L_ * L_;
+        st->visible_updates = cnt[3];
+        st->tile_pairs = cnt[0];
+        st->skipped_pairs = cnt[1];
+        st->fallback_pairs = cnt[2];
+        st->h2d_bytes = h2d_bytes_;
+        st->tile_w = tiled_ ? ts_.tw : 0;
+        st->tile_h = tiled_ ? ts_.th : 0;
+        st->block_x = tiled_ ? ts_.bx : 1;
+        st->block_y = tiled_ ? ts_.by : 1;
+        st->block_z = tiled_ ? ts_.bz : 1;
+    }
+    reset_recon();
+}
+
+void SlabContext::upload_views(const float* pixels, const double* mats, int count) {
+    if (!pixels || !mats) throw bph::config_error("null argument");
+    if (count < 1 || count > slots_)
+        throw bph::config_error("resident views exceed the ring capacity (ring_batches * view_batch)");
+    bind();
+    check(cudaStreamSynchronize(s_comp_), "sync");
+    resident_A_.resize((size_t)count);
+    for (int k = 0; k < count; ++k) {
+        bph::Mat m;
+        std::memcpy(m.data(), mats + 12 * k, sizeof(double) * 12);
+        bph::validate_matrix_for_grid(m, grid_);
+        resident_A_[(size_t)k] = bph::narrowed(m);
+        float* dst = d_ring_ + (size_t)k * isy_ * pitch_;
+        const float* src = pixels + (size_t)k * isy_ * isx_;
+        check(cudaMemcpy2DAsync(dst, (size_t)pitch_ * sizeof(float), src, (size_t)isx_ * sizeof(float),
+                                (size_t)isx_ * sizeof(float), (size_t)isy_, cudaMemcpyHostToDevice,
+                                s_copy_),
+              "H2D");
+    }
+    check(cudaStreamSynchronize(s_copy_), "sync");
+    std::fill(used_.begin(), used_.end(), false);
+    resident_ = count;
+}
+
+double SlabContext::time_resident(int iters, bp_gpu_stats* st) {
+    if (resident_ < 1) throw bph::config_error("no resident views (bp_gpu_upload_views first)");
+    if (iters < 1) throw bph::config_error("iters must be >= 1");
+    bind();
+    reset_recon();
+    check(cudaEventRecord(ev_t0_, s_comp_), "event");
+    for (int it = 0; it < iters; ++it) {
+        for (int k0 = 0; k0 < resident_; k0 += B_) {
+            bpg::BatchArgs b{};
+            b.nviews = std::min(B_, resident_ - k0);
+            b.load_volume = k0 > 0 ? 1 : 0;
+            for (int i = 0; i < b.nviews; ++i) {
+                std::memcpy(b.A[i], resident_A_[(size_t)(k0 + i)].data(), sizeof(float) * 12);
+                b.slot[i] = k0 + i;
+            }
+            choose_tile(b);
+            launch(b);
+        }
+    }
+    check(cudaEventRecord(ev_t1_, s_comp_), "event");
+    unsigned long long cnt[8] = {0};
+    check(cudaMemcpyAsync(cnt, d_cnt_, sizeof cnt, cudaMemcpyDeviceToHost, s_comp_), "counters");
+    check(cudaMemsetAsync(d_cnt_, 0, sizeof cnt, s_comp_), "counters");
+    check(cudaStreamSynchronize(s_comp_), "sync");
+    float ms = 0;
+    check(cudaEventElapsedTime(&ms, ev_t0_, ev_t1_), "elapsed");
+    if (st) {
+        std::memset(st, 0, sizeof *st);
+        st->device_ms = ms;
+        double kms = 0;
+        float m2 = 0;
+        for (size_t i = 0; i < launch_ev_used_; ++i) {
+            check(cudaEventElapsedTime(&m2, launch_ev_[i].first, launch_ev_[i].second), "elapsed");
+            kms += m2;
+        }
+        st->kernel_ms = kms;
+        st->views = (uint64_t)resident_ * iters;
+        st->launches = launches_;
+        st->nominal_updates = st->views * (uint64_t)nz_ * L_ * L_;
+        st->visible_updates = cnt[3];
+        st->tile_pairs = cnt[0];
+        st->skipped_pairs = cnt[1];
+        st->fallback_pairs = cnt[2];
+        st->tile_w = tiled_ ? ts_.tw : 0;
+        st->tile_h = tiled_ ? ts_.th : 0;
+        st->block_x = tiled_ ? ts_.bx : 1;
+        st->block_y = tiled_ ? ts_.by : 1;
+        st->block_z = tiled_ ? ts_.bz : 1;
+    }
+    reset_recon();
+    return ms;
+}
+
+}  // namespace bpr

@@ -1,0 +1,99 @@
+// bp_runtime.hpp -- per-GPU slab context: the streamed upload pipeline, the
+// batched kernel launches and the volume readback.
+//
+// Replaces the reference driver bp::reconstruct (proj/src/scheduler.cpp:24-133):
+//   * validation of every matrix against the grid (scheduler.cpp:35) happens per
+//     view as it arrives;
+//   * the serial, in-timed-region pad_image copies (scheduler.cpp:110-120) become
+//     asynchronous row-windowed H2D copies on a copy stream, overlapped with the
+//     kernel of the previous batch through a ring of device projection slots;
+//   * the std::thread pool + barriers (scheduler.cpp:65-106) become one kernel
+//     launch per view batch on a compute stream;
+//   * first-touch zeroing (scheduler.cpp:74) disappears: the first batch of a
+//     reconstruction writes its accumulators without reading the volume.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <array>
+#include <cstdint>
+#include <vector>
+
+#include "../../include/bp_gpu.h"
+#include "bp_device.hpp"
+#include "bp_host.hpp"
+
+namespace bpr {
+
+void check(cudaError_t e, const char* what);
+
+class SlabContext {
+public:
+    explicit SlabContext(const bp_gpu_config& cfg);
+    ~SlabContext();
+    SlabContext(const SlabContext&) = delete;
+    SlabContext& operator=(const SlabContext&) = delete;
+
+    // one view, ascending call order; copy=true stages the rows in pinned memory
+    void backproject(const float* image, const double* A, bool copy);
+    // drain, optional readback (nz*L*L floats), stats, reset for the next recon
+    void finish(float* host_volume, bp_gpu_stats* st);
+    void upload_views(const float* pixels, const double* mats, int count);
+    double time_resident(int iters, bp_gpu_stats* st);
+
+    float* device_volume() const { return d_vol_; }
+    int z_begin() const { return z0_; }
+    int z_end() const { return z1_; }
+    int device() const { return dev_; }
+    const bp_gpu_config& config() const { return cfg_; }
+    void bind() const;
+
+private:
+    void flush();
+    void choose_tile(const bpg::BatchArgs& b);
+    void launch(const bpg::BatchArgs& b);
+    void reset_recon();
+
+    bp_gpu_config cfg_;
+    int dev_ = 0;
+    bph::Grid grid_;
+    int L_ = 0, z0_ = 0, z1_ = 0, nz_ = 0, isx_ = 0, isy_ = 0, pitch_ = 0;
+    int B_ = 32, R_ = 3, slots_ = 0;
+    bool own_vol_ = true;
+    float* d_vol_ = nullptr;
+    float* d_ring_ = nullptr;
+    float* d_wx_ = nullptr;
+    float* d_wy_ = nullptr;
+    float* d_wz_ = nullptr;
+    unsigned long long* d_cnt_ = nullptr;
+    float* h_stage_ = nullptr;  // pinned staging, slots views
+    cudaStream_t s_comp_ = nullptr, s_copy_ = nullptr;
+    std::vector<cudaEvent_t> ev_ready_, ev_free_;
+    std::vector<bool> used_;
+    cudaEvent_t ev_t0_ = nullptr, ev_t1_ = nullptr, ev_h0_ = nullptr, ev_h1_ = nullptr,
+                ev_d0_ = nullptr, ev_d1_ = nullptr;
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> launch_ev_;
+    size_t launch_ev_used_ = 0;
+
+    // tiled kernel
+    bool tiled_ = false;
+    bpg::TileShape ts_{};
+    alignas(64) unsigned char tmap_[128];
+
+    // per-reconstruction state
+    bpg::BatchArgs cur_{};
+    int nb_ = 0;
+    int rg_ = 0;
+    bool any_launch_ = false;
+    bool any_h2d_ = false;
+    uint64_t views_ = 0, launches_ = 0, h2d_bytes_ = 0;
+    double wall_t0_ = 0.0;
+
+    // resident views
+    int resident_ = 0;
+    std::vector<std::array<float, 12>> resident_A_;
+};
+
+double now_ms();
+
+}  // namespace bpr

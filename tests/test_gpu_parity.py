@@ -1,0 +1,272 @@
+"""GPU parity: the sm_100a kernels against the CPU oracle (oracle/bp_oracle.c,
+itself pinned bitwise to the reference in tests/test_oracle.py).
+
+strict mode must be BITWISE identical to bp::reconstruct (proj/src/scheduler.cpp:24-133);
+fast mode must satisfy the north_star tolerance
+    max|d| <= 1e-4 * max|ref|   and   RMS <= 1e-6 * max|ref|.
+Known-answer cases port proj/tests/test_kernel.cpp:74-198.
+"""
+import numpy as np
+import pytest
+
+import paper_1104_5243_b200 as bp
+from oracle import oracle as O
+from tests.helpers import (TOL_MAX, TOL_RMS, baseline_small, bitwise_equal, err_stats,
+                           random_image, random_matrix, small_stack)
+
+pytestmark = pytest.mark.gpu
+
+
+def gpu_recon(px, mats, L, *, offset=(0.0, 0.0, 0.0), strict=True, kernel=0, view_batch=32,
+              distance_weight=True, copy=True, z_begin=0, z_end=0, count_visible=False,
+              row_windows=True):
+    n, isy, isx = px.shape
+    with bp.GpuContext(L, isx, isy, offset=offset, strict=strict, kernel=kernel,
+                       view_batch=view_batch, distance_weight=distance_weight, z_begin=z_begin,
+                       z_end=z_end, count_visible=count_visible, row_windows=row_windows) as ctx:
+        for k in range(n):
+            ctx.backproject(px[k], mats[k], copy=copy)
+        vol, st = ctx.finish()
+    return vol, st
+
+
+# ---- reciprocal -------------------------------------------------------------
+
+def test_rcp_pair_matches_frcp_rn():
+    # every float in [1, 2) and in [512, 1024) (w at the BASELINE geometry)
+    assert bp.selftest_rcp(0x3F800000, 0x40000000) == 0
+    assert bp.selftest_rcp(0x44000000, 0x44800000) == 0
+
+
+# ---- bitwise strict parity ------------------------------------------------------
+
+@pytest.mark.parametrize("L", [16, 24, 32, 48, 64])
+@pytest.mark.parametrize("kernel", [0, 1])
+def test_strict_bitwise_small_stack(L, kernel):
+    px, mats = small_stack("spheres3", 6, 64, 48)
+    ref, _ = O.reconstruct(px, mats, L)
+    got, st = gpu_recon(px, mats, L, kernel=kernel)
+    assert bitwise_equal(got, ref), err_stats(got, ref)
+
+
+@pytest.mark.parametrize("L", [32, 64, 128])
+def test_strict_bitwise_baseline_shaped(L):
+    px, mats = baseline_small(n_views=40, shrink=4)
+    ref, _ = O.reconstruct(px, mats, L)
+    got, st = gpu_recon(px, mats, L, strict=True)
+    assert st.fallback_pairs == 0
+    assert bitwise_equal(got, ref), err_stats(got, ref)
+
+
+def test_strict_bitwise_full_detector_128():
+    # config 1 geometry (1248x960 detector) on a reduced view count
+    px, mats = baseline_small(n_views=24, shrink=1)
+    ref, _ = O.reconstruct(px, mats, 128)
+    got, st = gpu_recon(px, mats, 128, strict=True)
+    assert st.tile_pairs > 0 and st.fallback_pairs == 0
+    assert bitwise_equal(got, ref), err_stats(got, ref)
+
+
+def test_strict_bitwise_offset_grid():
+    # config 5 shape: grid centre offset laterally (+60 mm), lines partly off-detector
+    px, mats = baseline_small(n_views=24, shrink=4)
+    ref, _ = O.reconstruct(px, mats, 64, offset=(60.0, 0.0, 0.0))
+    got, st = gpu_recon(px, mats, 64, offset=(60.0, 0.0, 0.0))
+    assert st.skipped_pairs > 0
+    assert bitwise_equal(got, ref), err_stats(got, ref)
+
+
+@pytest.mark.parametrize("view_batch", [1, 5, 32, 64])
+def test_batch_invariance(view_batch):
+    # projection blocking invariance (test_scheduler.cpp:63-133, acceptance C3)
+    px, mats = baseline_small(n_views=37, shrink=4)
+    ref, _ = O.reconstruct(px, mats, 64)
+    got, _ = gpu_recon(px, mats, 64, view_batch=view_batch)
+    assert bitwise_equal(got, ref)
+
+
+def test_plain_fx_switch():
+    # distance_weight = 0 (test_kernel.cpp:185-198)
+    px, mats = small_stack("shell", 5, 56, 48)
+    ref, _ = O.reconstruct(px, mats, 32, distance_weight=False)
+    for kernel in (0, 1):
+        got, _ = gpu_recon(px, mats, 32, distance_weight=False, kernel=kernel)
+        assert bitwise_equal(got, ref)
+
+
+# ---- fast mode tolerance ----------------------------------------------------------
+
+@pytest.mark.parametrize("L", [64, 128])
+def test_fast_within_tolerance(L):
+    px, mats = baseline_small(n_views=48, shrink=2)
+    ref, _ = O.reconstruct(px, mats, L)
+    got, _ = gpu_recon(px, mats, L, strict=False)
+    emax, erms = err_stats(got, ref)
+    assert emax <= TOL_MAX and erms <= TOL_RMS, (emax, erms)
+
+
+# ---- known answers (test_kernel.cpp) ------------------------------------------------
+
+def _single_view(img, A, L, **kw):
+    return gpu_recon(img[None], np.asarray(A, np.float64)[None], L, **kw)[0]
+
+
+def test_zero_image_noop():
+    img = np.zeros((64, 64), np.float32)
+    A = random_matrix(17, 64, 64)
+    vol = _single_view(img, A, 32)
+    assert not vol.any()
+
+
+def test_pixel_centre_hits_accumulate_c_r2():
+    # test_kernel.cpp:84-101: u = x-ish, v on a pixel centre, w = 1
+    L = 256
+    g = O.Grid.cube(L)
+    wz136 = g.oz + 136 * g.MM
+    A = [1, 0, 0, 0, 1, 0, 0, 0, 0, 127.5, 127.5 - wz136, 1]
+    c = 0.8125
+    img = np.full((32, 32), c, np.float32)
+    for kernel in (0, 1):
+        vol = _single_view(img, A, L, kernel=kernel)
+        line = vol[136, 130]
+        for x in range(128, 141):
+            u = np.float32(g.ox + x * g.MM) + np.float32(127.5)
+            if u == np.floor(u) and 0 <= u < 31:
+                assert line[x] == np.float32(c)
+        ref = np.zeros(L, np.float32)
+        O.line_update(ref, img, np.asarray(A, np.float32), L, 130, 136, 0, L - 1)
+        assert bitwise_equal(line, ref)
+
+
+def test_fully_outside_contributes_exact_zero():
+    # test_kernel.cpp:151-167: u = wx + 5000, far off-detector for every voxel
+    img = random_image(32, 32, 55, 0.5, 2.0)
+    A = [1, 0, 0, 0, 1, 0, 0, 0, 0, 5000.0, 0.0, 1.0]
+    for kernel in (0, 1):
+        vol = _single_view(img, A, 16, kernel=kernel)
+        assert not vol.any()
+
+
+def test_partially_outside_matches_guarded_double_oracle():
+    # test_kernel.cpp:169-183: the projected line straddles the left image edge
+    img = random_image(24, 24, 77, 0.5, 1.5)
+    A = [0.125, 0, 0, 0, 0, 0, 0, 0.0, 0, 10.0, 12.3, 1.0]
+    L = 32
+    vol = _single_view(img, A, L)
+    g = O.Grid.cube(L)
+    f = np.asarray(A, np.float32).astype(np.float64)
+    wy, wz = g.oy + 4 * g.MM, g.oz + 4 * g.MM
+    for x in range(L):
+        wx = g.ox + x * g.MM
+        uw = f[0] * wx + f[3] * wy + f[6] * wz + f[9]
+        vw = f[1] * wx + f[4] * wy + f[7] * wz + f[10]
+        w = f[2] * wx + f[5] * wy + f[8] * wz + f[11]
+        u, v = uw / w, vw / w
+        iu, iv = int(np.floor(u)), int(np.floor(v))
+        sx, sy = u - iu, v - iv
+
+        def pix(a, b):
+            return float(img[b, a]) if 0 <= a < 24 and 0 <= b < 24 else 0.0
+        fx = sx * (sy * pix(iu + 1, iv + 1) + (1 - sy) * pix(iu + 1, iv)) + \
+            (1 - sx) * (sy * pix(iu, iv + 1) + (1 - sy) * pix(iu, iv))
+        ref = fx / (w * w)
+        assert abs(vol[4, 4, x] - ref) <= 1e-5 * max(1.0, abs(ref))
+
+
+# ---- clip statistics ------------------------------------------------------------------
+
+def test_visible_update_count_matches_clip_stats():
+    px, mats = baseline_small(n_views=16, shrink=4)
+    for L in (32, 64):
+        ref = int(O.visible_updates(mats, px.shape[2], px.shape[1], L).sum())
+        _, st = gpu_recon(px, mats, L, count_visible=True)
+        assert st.visible_updates == ref
+        if O.ref_available():
+            assert ref == O.ref_clip_total(mats, px.shape[2], px.shape[1], L)
+
+
+# ---- pipeline / API invariance -----------------------------------------------------
+
+def test_copy_and_async_paths_identical():
+    px, mats = baseline_small(n_views=20, shrink=4)
+    a, _ = gpu_recon(px, mats, 64, copy=True)
+    b, _ = gpu_recon(px, mats, 64, copy=False)
+    assert bitwise_equal(a, b)
+
+
+def test_bp_reconstruct_drop_in():
+    # reference C ABI (capi.cpp:109-166) through the GPU
+    px, mats = small_stack("spheres3", 4, 48, 40)
+    st = bp.Stack.from_arrays(px, mats)
+    vol, rs = bp.reconstruct(st, bp.recon_params(16, block_b=1))
+    ref, _ = O.reconstruct(px, mats, 16)
+    assert bitwise_equal(vol.data, ref)
+    assert rs.voxel_updates == 4 * 16 ** 3
+    assert rs.writeback_stores == 4 * 16 ** 3
+    assert rs.gflops == pytest.approx(31.0 * rs.gups)
+    # repeat: cached context, fresh volume
+    vol2, _ = bp.reconstruct(st, bp.recon_params(16, block_b=3))
+    assert bitwise_equal(vol2.data, ref)
+
+
+def test_slab_and_virtual_slabs_equal_full():
+    px, mats = baseline_small(n_views=24, shrink=4)
+    stack = bp.Stack.from_arrays(px, mats)
+    full, _ = bp.reconstruct_ex(stack, 64)
+    for G in (2, 3, 5):
+        got, st = bp.reconstruct_ex(stack, 64, virtual_slabs=G)
+        assert bitwise_equal(got, full), G
+        assert st.h2d_bytes <= G * px.nbytes
+    ref, _ = O.reconstruct(px, mats, 64)
+    assert bitwise_equal(full, ref)
+
+
+def test_explicit_slab_context():
+    px, mats = baseline_small(n_views=12, shrink=4)
+    ref, _ = O.reconstruct(px, mats, 64, z0=20, z1=41)
+    got, st = gpu_recon(px, mats, 64, z_begin=20, z_end=41)
+    assert got.shape == (21, 64, 64)
+    assert bitwise_equal(got, ref)
+    assert st.h2d_bytes < px.nbytes  # row windows trimmed the upload
+
+
+def test_determinism_repeat():
+    px, mats = baseline_small(n_views=16, shrink=4)
+    a, _ = gpu_recon(px, mats, 64, strict=False)
+    b, _ = gpu_recon(px, mats, 64, strict=False)
+    assert bitwise_equal(a, b)
+
+
+def test_resident_timing_path_matches_streaming():
+    px, mats = baseline_small(n_views=40, shrink=4)
+    n, isy, isx = px.shape
+    with bp.GpuContext(64, isx, isy, ring_batches=2, view_batch=32) as ctx:
+        ctx.upload_views(px, mats)
+        ms, st = ctx.time_resident(iters=2)
+        assert ms > 0 and st.views == 2 * n
+        ptr = ctx.volume_device_ptr()
+        assert ptr != 0
+        vol, _ = ctx.finish()  # no views queued: volume keeps the resident result? (reset)
+    ref, _ = O.reconstruct(px, mats, 64)
+    got, _ = gpu_recon(px, mats, 64)
+    assert bitwise_equal(got, ref)
+
+
+def test_invalid_geometry_rejected():
+    px, mats = small_stack("point", 2, 24, 24)
+    bad = mats.copy()
+    bad[1] = [1, 0, 0, 0, 1, 0, 0, 0, 0, 0, 0, -1]
+    with pytest.raises(bp.BPError) as e:
+        gpu_recon(px, bad, 8)
+    assert e.value.code == bp.BP_EVERIFY
+
+
+def test_approx_recip_modes_match_reference_ladder():
+    # recip.hpp:14-23 restated on the GPU (simple kernel); PSNR ordering of acceptance C4
+    px, mats = small_stack("spheres3", 4, 48, 40)
+    st = bp.Stack.from_arrays(px, mats)
+    exact, _ = bp.reconstruct(st, bp.recon_params(16))
+    nr, _ = bp.reconstruct(st, bp.recon_params(16, recip_mode=bp.BP_RECIP_APPROX12_NR))
+    ap, _ = bp.reconstruct(st, bp.recon_params(16, recip_mode=bp.BP_RECIP_APPROX12))
+    p_nr, p_12 = nr.psnr(exact), ap.psnr(exact)
+    assert p_nr >= 90.0 and p_12 <= p_nr - 20.0 and p_12 > 20.0
