@@ -38,6 +38,7 @@ struct SlabArgs {
     int isx, isy;                // detector size
     int pitch;                   // row pitch of a projection slot, floats (multiple of 4)
     int nbx, nby, nbz;           // voxel blocks of the tiled kernel
+    int debug;                   // BP_DEBUG bits (diagnostics only)
 };
 
 // Launchers (bp_kernels.cu).  All asynchronous on `stream`.

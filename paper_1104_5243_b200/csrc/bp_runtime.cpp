@@ -4,6 +4,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 
@@ -229,14 +230,21 @@ void SlabContext::choose_tile(const bpg::BatchArgs& b) {
                     if (!(wmin > 0) || std::fabs(umin) > 1e6 || std::fabs(umax) > 1e6 ||
                         std::fabs(vmin) > 1e6 || std::fabs(vmax) > 1e6)
                         continue;
-                    const int iu0 = (int)std::floor(umin) - 1, iu1 = (int)std::floor(umax) + 2;
+                    const int iu0 = ((int)std::floor(umin) - 1) & ~3;  // 16 B aligned origin
+                    const int iu1 = (int)std::floor(umax) + 2;
                     const int iv0 = (int)std::floor(vmin) - 1, iv1 = (int)std::floor(vmax) + 2;
                     if (iu1 < 0 || iu0 > isx_ - 1 || iv1 < 0 || iv0 > isy_ - 1) continue;
                     need_w = std::max(need_w, iu1 - iu0 + 1);
                     need_h = std::max(need_h, iv1 - iv0 + 1);
                 }
     }
-    int tw = round_up(std::max(need_w, 8) + 8, 4);
+    // Row pitch of the SMEM tile == TMA box width.  Pitches == 20 (mod 32) floats
+    // minimise bank conflicts of the 8x4 lane layout (scratch/bank_sim.py).
+    int tw = round_up(std::max(need_w, 8) + 4, 4);
+    if (tw % 32 != 20) {
+        const int t2 = tw + ((20 - tw % 32) + 32) % 32;
+        if (t2 <= 256) tw = t2;
+    }
     int th = round_up(std::max(need_h, 8) + 8, 8);
     tw = std::min(tw, 256);
     th = std::min(th, 256);
@@ -271,6 +279,7 @@ void SlabContext::launch(const bpg::BatchArgs& b) {
     s.isx = isx_;
     s.isy = isy_;
     s.pitch = pitch_;
+    if (const char* d = std::getenv("BP_DEBUG")) s.debug = std::atoi(d);
     if (tiled_) {
         s.nbx = (L_ + ts_.bx - 1) / ts_.bx;
         s.nby = (L_ + ts_.by - 1) / ts_.by;
