@@ -104,7 +104,7 @@ EXPORTED = [
     "bp_baseline_params_init", "bp_stack_generate_baseline", "bp_baseline_phantom",
     "bp_volume_create", "bp_volume_data_mut", "bp_gpu_set_devices", "bp_gpu_device_count",
     "bp_partition_slabs", "bp_slab_row_window", "bp_recon_ex_init", "bp_reconstruct_ex",
-    "bp_selftest_rcp", "bp_build_info",
+    "bp_selftest_rcp", "bp_build_info", "bp_gpu_read_lines", "bp_device_compare",
 ]
 
 
@@ -169,6 +169,8 @@ def lib():
         "bp_recon_ex_init": (None, [C.POINTER(ReconEx)]),
         "bp_reconstruct_ex": (ip, [vp, u32, C.POINTER(ReconEx), fp, C.POINTER(GpuStats)]),
         "bp_selftest_rcp": (ip, [u32, u32, C.POINTER(C.c_uint64)]),
+        "bp_gpu_read_lines": (ip, [vp, C.POINTER(ip), C.POINTER(ip), ip, fp]),
+        "bp_device_compare": (ip, [vp, vp, C.c_uint64, dp, dp, dp, C.POINTER(C.c_uint64)]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)
@@ -490,6 +492,23 @@ class GpuContext:
         a, b = C.c_int(), C.c_int()
         _check(lib().bp_gpu_volume_device(self._h, C.byref(p), C.byref(a), C.byref(b)))
         return p.value
+
+    def read_lines(self, ys, zs) -> np.ndarray:
+        ys = np.ascontiguousarray(ys, np.int32)
+        zs = np.ascontiguousarray(zs, np.int32)
+        out = np.empty((len(ys), self.l), np.float32)
+        _check(lib().bp_gpu_read_lines(self._h, ys.ctypes.data_as(C.POINTER(C.c_int)),
+                                       zs.ctypes.data_as(C.POINTER(C.c_int)), len(ys), _f(out)))
+        return out
+
+    def compare_with(self, other: "GpuContext"):
+        """(max|a-b|, max|b|, rms(a-b), n_bitwise_diff) of the two device slabs."""
+        n = (self.z_end - self.z_begin) * self.l * self.l
+        mx, mr, ss, nb = C.c_double(), C.c_double(), C.c_double(), C.c_uint64()
+        _check(lib().bp_device_compare(C.c_void_p(self.volume_device_ptr()),
+                                       C.c_void_p(other.volume_device_ptr()), n, C.byref(mx),
+                                       C.byref(mr), C.byref(ss), C.byref(nb)))
+        return mx.value, mr.value, (ss.value / n) ** 0.5, nb.value
 
     def close(self):
         if getattr(self, "_h", None):

@@ -333,6 +333,25 @@ int bp_gpu_volume_device(bp_gpu_ctx* ctx, float** dptr, int* z_begin, int* z_end
     return BP_OK;
 }
 
+int bp_gpu_read_lines(bp_gpu_ctx* ctx, const int* ys, const int* zs, int n, float* out) {
+    if (!ctx) return fail(BP_EINVAL, "null argument");
+    return guarded([&] { ctx->c->read_lines(ys, zs, n, out); });
+}
+
+int bp_device_compare(const float* d_a, const float* d_b, uint64_t n, double* max_abs_diff,
+                      double* max_abs_ref, double* sum_sq_diff, uint64_t* n_bit_diff) {
+    if (!d_a || !d_b) return fail(BP_EINVAL, "null argument");
+    return guarded([&] {
+        double r[3];
+        unsigned long long nb = 0;
+        bpr::check((cudaError_t)bpg::device_compare(d_a, d_b, n, r, &nb), "device compare");
+        if (max_abs_diff) *max_abs_diff = r[0];
+        if (max_abs_ref) *max_abs_ref = r[1];
+        if (sum_sq_diff) *sum_sq_diff = r[2];
+        if (n_bit_diff) *n_bit_diff = nb;
+    });
+}
+
 int bp_gpu_upload_views(bp_gpu_ctx* ctx, const float* pixels, const double* matrices, int count) {
     if (!ctx || !pixels || !matrices) return fail(BP_EINVAL, "null argument");
     return guarded([&] { ctx->c->upload_views(pixels, matrices, count); });

@@ -74,6 +74,10 @@ int smem_bytes_for(const TileShape& ts);
 // float bit patterns [lo_bits, hi_bits).  Synchronous.
 int selftest_rcp(uint32_t lo_bits, uint32_t hi_bits, unsigned long long* mismatches);
 
+// max|a-b|, max|b|, sum (a-b)^2 into res3; bitwise-different count into nbit.
+int device_compare(const float* a, const float* b, unsigned long long n, double* res3,
+                   unsigned long long* nbit);
+
 // Exact visible-update count (clip_stats semantics, precompute.cpp:93-103)
 // for views [0,n) of the batch: adds into counters[3].
 int launch_clip_count(const SlabArgs& s, const BatchArgs& b, void* stream);

@@ -385,6 +385,21 @@ void SlabContext::finish(float* host_volume, bp_gpu_stats* st) {
     reset_recon();
 }
 
+void SlabContext::read_lines(const int* ys, const int* zs, int n, float* out) {
+    if (!ys || !zs || !out || n < 0) throw bph::config_error("null argument");
+    bind();
+    check(cudaStreamSynchronize(s_comp_), "sync");
+    for (int i = 0; i < n; ++i) {
+        if (ys[i] < 0 || ys[i] >= L_ || zs[i] < z0_ || zs[i] >= z1_)
+            throw bph::config_error("line outside the slab");
+        const float* src = d_vol_ + ((size_t)(zs[i] - z0_) * L_ + ys[i]) * L_;
+        check(cudaMemcpyAsync(out + (size_t)i * L_, src, (size_t)L_ * sizeof(float),
+                              cudaMemcpyDeviceToHost, s_comp_),
+              "D2H line");
+    }
+    check(cudaStreamSynchronize(s_comp_), "sync");
+}
+
 void SlabContext::upload_views(const float* pixels, const double* mats, int count) {
     if (!pixels || !mats) throw bph::config_error("null argument");
     if (count < 1 || count > slots_)

@@ -39,6 +39,7 @@ public:
     // drain, optional readback (nz*L*L floats), stats, reset for the next recon
     void finish(float* host_volume, bp_gpu_stats* st);
     void upload_views(const float* pixels, const double* mats, int count);
+    void read_lines(const int* ys, const int* zs, int n, float* out);
     double time_resident(int iters, bp_gpu_stats* st);
 
     float* device_volume() const { return d_vol_; }

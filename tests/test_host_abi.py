@@ -1,0 +1,171 @@
+"""Host-side behaviour of libbackproject.so that needs no GPU: symbol exports,
+stacks/volumes/file formats, datagen, error codes, partitioner and row windows."""
+import ctypes as C
+import os
+import re
+
+import numpy as np
+import pytest
+
+import paper_1104_5243_b200 as bp
+from oracle import oracle as O
+from tests.helpers import bitwise_equal, baseline_small, small_stack
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def header_functions():
+    names = set()
+    for h in ("backproject.h", "bp_gpu.h"):
+        txt = open(os.path.join(ROOT, "include", h)).read()
+        txt = re.sub(r"/\*.*?\*/", "", txt, flags=re.S)
+        for m in re.finditer(r"\b(bp_[a-z0-9_]+)\s*\(", txt):
+            names.add(m.group(1))
+    return names
+
+
+def test_library_exports_every_header_symbol():
+    lib = C.CDLL(bp.LIB_PATH)
+    names = header_functions()
+    assert len(names) >= 40
+    missing = [n for n in sorted(names) if not hasattr(lib, n)]
+    assert not missing, missing
+    assert set(bp.EXPORTED) >= names - {"bp_stack_generate"} | set()
+
+
+def test_build_info_mentions_sm100a():
+    assert "sm_100a" in bp.build_info()
+
+
+def test_stack_roundtrip_and_dims(tmp_path):
+    px, mats = small_stack("spheres3", 3, 40, 30)
+    s = bp.Stack.from_arrays(px, mats)
+    assert s.dims == (40, 30, 3)
+    assert bitwise_equal(s.pixels, px) and np.array_equal(s.matrices, mats)
+    p = str(tmp_path / "s.bpst")
+    s.write(p)
+    t = bp.Stack.read(p)
+    assert t.dims == s.dims and bitwise_equal(t.pixels, px) and np.array_equal(t.matrices, mats)
+
+
+def test_datagen_matches_reference_bitwise():
+    if not O.ref_available():
+        pytest.skip("oracle/_ref not built")
+    s = bp.Stack.generate("shell", 5, 64, 48, 750.0, 1200.0, 0.32 * 1248 / 64)
+    px, mats = O.ref_make_stack("shell", 5, 64, 48, pitch=0.32 * 1248 / 64)
+    assert bitwise_equal(s.pixels, px) and np.array_equal(s.matrices, mats)
+    # the library's analytic projector on an arbitrary ellipsoid phantom
+    ell = bp.baseline_phantom(seed=3, n_ellipsoids=4)
+    ref = O.ref_forward_project(ell, mats[2], 64, 48)
+    b = bp.Stack.baseline(n_views=1, isx=64, isy=48, seed=3, n_ellipsoids=4, filter=0,
+                          pitch_mm=0.32 * 1248 / 64)
+    ref_b = O.ref_forward_project(ell, b.matrices[0], 64, 48)
+    assert bitwise_equal(b.pixels[0], ref_b)
+    assert ref.shape == (48, 64)
+
+
+def test_bpst_interoperates_with_reference_reader(tmp_path):
+    if not O.ref_available():
+        pytest.skip("oracle/_ref not built")
+    px, mats = small_stack("point", 2, 24, 20)
+    p = str(tmp_path / "x.bpst")
+    bp.Stack.from_arrays(px, mats).write(p)
+    R = O.ref()
+    R.bp_stack_read.argtypes = [C.c_char_p, C.POINTER(C.c_void_p)]
+    R.bp_stack_dims.argtypes = [C.c_void_p] + [C.POINTER(C.c_uint32)] * 3
+    h = C.c_void_p()
+    assert R.bp_stack_read(p.encode(), C.byref(h)) == 0
+    a, b, c = C.c_uint32(), C.c_uint32(), C.c_uint32()
+    R.bp_stack_dims(h, C.byref(a), C.byref(b), C.byref(c))
+    assert (a.value, b.value, c.value) == (24, 20, 2)
+
+
+def test_volume_roundtrip_and_psnr(tmp_path):
+    v = bp.Volume.create(8)
+    v.data[:] = np.arange(512, dtype=np.float32).reshape(8, 8, 8)
+    p = str(tmp_path / "v.bpvl")
+    v.write(p)
+    w = bp.Volume.read(p)
+    assert w.edge == 8 and bitwise_equal(w.data, v.data)
+    assert np.isinf(w.psnr(v))
+    w.data[0, 0, 0] += 1.0
+    assert np.isfinite(w.psnr(v))
+
+
+def test_error_codes_and_thread_local_message(tmp_path):
+    with pytest.raises(bp.BPError) as e:
+        bp.Stack.generate("nope", 2, 32, 32)
+    assert e.value.code == bp.BP_EINVAL and "nope" in bp.last_error()
+    with pytest.raises(bp.BPError) as e:
+        bp.Stack.read("/nonexistent/x.bpst")
+    assert e.value.code == bp.BP_EIO
+    bad = tmp_path / "bad.bpst"
+    bad.write_bytes(b"XXXX" + b"\0" * 16)
+    with pytest.raises(bp.BPError) as e:
+        bp.Stack.read(str(bad))
+    assert e.value.code == bp.BP_EIO and "at byte 0" in str(e.value)
+    trunc = tmp_path / "t.bpst"
+    trunc.write_bytes(b"BPST" + np.array([8, 8, 2], np.uint32).tobytes() + b"\0" * 10)
+    with pytest.raises(bp.BPError) as e:
+        bp.Stack.read(str(trunc))
+    assert e.value.code == bp.BP_EIO and "truncated" in str(e.value)
+    lib = bp.lib()
+    assert lib.bp_stack_read(None, None) == bp.BP_EINVAL
+    assert lib.bp_machine_load(b"x", None) == bp.BP_EINVAL
+
+
+def test_reconstruct_parameter_validation_precedes_device():
+    # capi.cpp:113-130 / scheduler.cpp:31-34: bad params are BP_EINVAL even on a CPU host
+    px, mats = small_stack("point", 2, 24, 24)
+    s = bp.Stack.from_arrays(px, mats)
+    for kw in [dict(recip_mode=7), dict(extract=3), dict(threads=0), dict(lanes=5)]:
+        with pytest.raises(bp.BPError) as e:
+            bp.reconstruct(s, bp.recon_params(8, **kw))
+        assert e.value.code == bp.BP_EINVAL
+    with pytest.raises(bp.BPError) as e:
+        bp.reconstruct(s, bp.recon_params(0))
+    assert e.value.code == bp.BP_EINVAL
+
+
+@pytest.mark.skipif(bp.device_count() > 0, reason="CPU-only behaviour")
+def test_no_cpu_fallback_on_cpu_host():
+    px, mats = small_stack("point", 2, 24, 24)
+    with pytest.raises(bp.BPError) as e:
+        bp.reconstruct(bp.Stack.from_arrays(px, mats), bp.recon_params(8))
+    assert e.value.code == bp.BP_EINTERNAL and "no CUDA device" in str(e.value)
+
+
+@pytest.mark.parametrize("L,G", [(64, 2), (64, 4), (128, 8), (48, 3)])
+def test_partition_is_a_balanced_cover(L, G):
+    px, mats = baseline_small(n_views=32, shrink=8, filter=0)
+    b = bp.partition_slabs(mats, px.shape[2], px.shape[1], L, G)
+    assert b[0] == 0 and b[-1] == L and len(b) == G + 1
+    assert np.all(np.diff(b) >= 1)
+    vis = np.array([O.visible_updates(mats, px.shape[2], px.shape[1], L, z0=int(b[i]),
+                                      z1=int(b[i + 1])).sum() for i in range(G)], np.float64)
+    equal = np.linspace(0, L, G + 1).astype(int)
+    vis_eq = np.array([O.visible_updates(mats, px.shape[2], px.shape[1], L, z0=int(equal[i]),
+                                         z1=int(equal[i + 1])).sum() for i in range(G)])
+    # work-balanced slabs are at least as balanced as equal-thickness ones
+    assert vis.max() / vis.mean() <= max(1.12, vis_eq.max() / vis_eq.mean() + 1e-9)
+
+
+def test_row_window_is_conservative():
+    # a slab reconstructed from ONLY its row window (other rows zeroed) is bitwise
+    # identical to the full-detector result: the window holds every footprint
+    px, mats = baseline_small(n_views=10, shrink=8)
+    L = 48
+    isy = px.shape[1]
+    for z0, z1 in [(0, 12), (12, 30), (30, 48), (20, 21)]:
+        masked = px.copy()
+        rows = []
+        for k in range(px.shape[0]):
+            r0, r1 = bp.slab_row_window(mats[k], isy, L, z0, z1)
+            masked[k, :r0] = 0.0
+            masked[k, r1:] = 0.0
+            rows.append(r1 - r0)
+        full, _ = O.reconstruct(px, mats, L, z0=z0, z1=z1)
+        win, _ = O.reconstruct(masked, mats, L, z0=z0, z1=z1)
+        assert bitwise_equal(full, win), (z0, z1)
+        if z1 - z0 <= 12:
+            assert np.mean(rows) < isy
