@@ -19,7 +19,7 @@ import subprocess
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libbackproject.so")
+LIB_PATH = os.environ.get("BP_LIB_PATH") or os.path.join(HERE, "libbackproject.so")
 
 BP_OK, BP_EINVAL, BP_EIO, BP_EVERIFY, BP_EINTERNAL = 0, 1, 2, 3, 4
 BP_RECIP_EXACT, BP_RECIP_APPROX12, BP_RECIP_APPROX12_NR = 0, 1, 2

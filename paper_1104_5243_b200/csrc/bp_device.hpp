@@ -48,6 +48,7 @@ struct TileShape {
     int bx, by, bz;              // voxel block
     int tw, th;                  // tile capacity (floats), tw % 4 == 0, th % 8 == 0
     int stages;
+    int zp;                      // 1: z-paired thread layout
     int threads;                 // consumer + producer threads per CTA
     int smem_bytes;
 };

@@ -241,7 +241,14 @@ void SlabContext::choose_tile(const bpg::BatchArgs& b) {
     // Row pitch of the SMEM tile == TMA box width.  Pitches == 20 (mod 32) floats
     // minimise bank conflicts of the 8x4 lane layout (scratch/bank_sim.py).
     int tw = round_up(std::max(need_w, 8) + 4, 4);
-    if (tw % 32 != 20) {
+    const bool twc_ok = !std::getenv("BP_NO_TWC") && t.stages == 2 &&
+                        ((t.bx == 32 && t.bz == 8) || (t.bx == 16 && t.bz == 16));
+    if (t.bx == 32 && t.zp && tw <= 144 && twc_ok) tw = 144;
+    if (twc_ok && t.bx == 16 && tw <= 80) {
+        tw = 80;   // compile-time pitch 64+16
+    } else if (twc_ok && tw <= 144) {
+        tw = 144;  // compile-time pitch 128+16: ALU-only texel addressing, low conflicts
+    } else if (tw % 32 != 20) {
         const int t2 = tw + ((20 - tw % 32) + 32) % 32;
         if (t2 <= 256) tw = t2;
     }
