@@ -177,13 +177,23 @@ def run_reference_arm(args):
 # ---------------------------------------------------------------------------
 # our arm
 
+def _load_profile_summary():
+    try:
+        with open(os.path.join(ROOT, "profiles", "latest.json")) as f:
+            return json.load(f)
+    except Exception:
+        return {}
+
+
 def run_ours(args):
     import paper_1104_5243_b200 as bp
     rank, world, local = dist_env()
-    dist = None
+    dist = torch = None
     if world > 1:
-        import torch.distributed as dist  # plumbing only: barrier + max-reduce of timings
-        dist.init_process_group("gloo")
+        import torch
+        import torch.distributed as dist  # plumbing: barrier, max-reduce, slab gather
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     n_dev = bp.device_count()
     if n_dev < 1:
         print(json.dumps({"metric": METRIC, "error": "no CUDA device"}))
@@ -199,8 +209,8 @@ def run_ours(args):
         bounds = bp.partition_slabs(mats, isx, isy, L, world)
         z0, z1 = int(bounds[rank]), int(bounds[rank + 1])
     else:
+        bounds = [0, L]
         z0, z1 = 0, L
-    nz = z1 - z0
 
     # ---- visible updates (clip_stats semantics) for the roofline -------------
     with bp.GpuContext(L, isx, isy, device=device, z_begin=z0, z_end=z1, count_visible=True,
@@ -211,33 +221,72 @@ def run_ours(args):
 
     # ---- value: resident projections, device-event timing ---------------------
     ring = (n + args.batch - 1) // args.batch
+    slab_t = full_t = None
+    if world > 1:
+        # the slab volume is a torch tensor so the gather can use NCCL directly;
+        # rank 0's slab is a view into the full volume (no extra copy)
+        if rank == 0:
+            full_t = torch.empty((L, L, L), dtype=torch.float32, device="cuda")
+            slab_t = full_t[z0:z1]
+        else:
+            slab_t = torch.empty((z1 - z0, L, L), dtype=torch.float32, device="cuda")
     ctx = bp.GpuContext(L, isx, isy, device=device, z_begin=z0, z_end=z1, strict=args.strict,
-                        view_batch=args.batch, ring_batches=ring, profile_launches=True)
+                        view_batch=args.batch, ring_batches=ring, profile_launches=True,
+                        device_volume=slab_t.data_ptr() if slab_t is not None else None)
     ctx.upload_stack(stack)
-    if args.warmup:
-        ctx.time_resident(args.warmup)
+
+    def gather_ms():
+        """The single exchange step: variable-size slabs to rank 0 over NCCL."""
+        if world == 1:
+            return 0.0
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record()
+        if rank == 0:
+            for src in range(1, world):
+                dist.recv(full_t[int(bounds[src]):int(bounds[src + 1])], src=src)
+        else:
+            dist.send(slab_t, dst=0)
+        e1.record()
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1)
+
+    for _ in range(args.warmup):
+        ctx.time_resident(1)
+        gather_ms()
     if dist:
         dist.barrier()
     clk = ClockSampler(device)
     clk.start()
-    ms, st = ctx.time_resident(args.steps)
+    ms = 0.0
+    launches = 0
+    kernel_ms = 0.0
+    st = None
+    for _ in range(args.steps):
+        m, st = ctx.time_resident(1)
+        ms += m + gather_ms()
+        launches += int(st.launches)
+        kernel_ms += float(st.kernel_ms)
     clocks = clk.stop()
     if dist:
-        import torch
-        t = torch.tensor([ms], dtype=torch.float64)
+        t = torch.tensor([ms], dtype=torch.float64, device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
+        t = torch.tensor([launches], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        total_launches = int(t.item())
+    else:
+        total_launches = launches
     nominal_step = n * L ** 3  # whole job, all ranks
     value = nominal_step * args.steps / (ms / 1e3) / 1e9
-    launches = int(st.launches)
-    kernel_ms = float(st.kernel_ms)
     per_launch_s = kernel_ms / 1e3 / max(1, launches)
+    launches_per_step = launches / args.steps
     ctx.close()
 
     # ---- e2e: streamed through the C ABI from pinned host memory ---------------
     e2e_ctx = bp.GpuContext(L, isx, isy, device=device, z_begin=z0, z_end=z1,
                             strict=args.strict, view_batch=args.batch, ring_batches=3)
-    host_vol = bp.Volume.create(L)  # pinned (library pool)
+    host_vol = bp.Volume.create(L)  # pinned (library pool); each rank reads back its slab
     out = host_vol.data[z0:z1]
     for _ in range(max(1, args.warmup)):
         e2e_ctx.backproject_stack(stack)
@@ -246,17 +295,21 @@ def run_ours(args):
         dist.barrier()
     t0 = time.perf_counter()
     h2d = d2h = 0
+    h2d_ms = d2h_ms = 0.0
     for _ in range(args.steps):
         e2e_ctx.backproject_stack(stack)
         _, est = e2e_ctx.finish(out=out)
         h2d += est.h2d_bytes
         d2h += est.d2h_bytes
+        h2d_ms += est.h2d_ms
+        d2h_ms += est.d2h_ms
     e2e_s = time.perf_counter() - t0
     if dist:
-        import torch
-        t = torch.tensor([e2e_s], dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_s = float(t.item())
+        t = torch.tensor([e2e_s, h2d, d2h], dtype=torch.float64, device="cuda")
+        mx = t.clone()
+        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        e2e_s, h2d, d2h = float(mx[0].item()), int(t[1].item()), int(t[2].item())
     e2e_ctx.close()
     e2e_val = nominal_step * args.steps / e2e_s / 1e9
 
@@ -269,16 +322,22 @@ def run_ours(args):
                "sample": f"{args.cpu_views} of {n} views over the full {L}^3 volume "
                          f"(bp::reconstruct lanes=8 block_b=8 clip=1; wall {r['wall_s']:.2f} s)"}
 
+    if dist:
+        vt = torch.tensor([visible], dtype=torch.float64, device="cuda")
+        dist.all_reduce(vt, op=dist.ReduceOp.SUM)
+        visible_all = int(vt.item())
+    else:
+        visible_all = visible
     if rank != 0:
+        dist.destroy_process_group()
         return 0
     peaks = load_peaks()
+    prof = _load_profile_summary()
     sm_mhz = clocks.get("sm_mhz") or peaks.get("sm_max_mhz", 1965.0)
     sm_max = clocks.get("sm_max_mhz") or peaks.get("sm_max_mhz", 1965.0)
     # dominant kernel: tiled backprojection.  Algorithmic SMEM-load bytes per launch =
     # 16 B x visible updates per launch (4 fp32 texels per update).
-    vis_per_launch = visible * world / max(1, (launches / args.steps))
-    achieved = 16.0 * (visible / max(1, launches / args.steps)) / per_launch_s / 1e9 if world == 1 \
-        else 16.0 * vis_per_launch / per_launch_s / 1e9
+    achieved = 16.0 * (visible / max(1e-9, launches_per_step)) / per_launch_s / 1e9
     peak_nominal = SMEM_BYTES_PER_SM_CLK * N_SM * float(sm_max) * 1e6 / 1e9
     line = {
         "metric": METRIC, "value": value, "unit": "GUP/s", "n_gpus": world, "steps": args.steps,
@@ -286,21 +345,27 @@ def run_ours(args):
         "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {"workload": f"{L}^3 x {n} views of 1248x960 (BASELINE config 3)", "l": L,
                    "views": n, "view_batch": args.batch,
-                   "arithmetic": "fast (FMA lerp)" if not args.strict else "strict (bitwise)",
-                   "l2": "inputs larger than L2 (2.38 GB stack + 512 MiB volume)",
-                   "parallelism": f"z-slab x{world}"},
-        "gpu_launches": launches,
-        "visible_updates_per_step": visible * (world if world > 1 else 1),
-        "gups_visible": visible * args.steps / (ms / 1e3) / 1e9,
+                   "arithmetic": "strict (bitwise reference)" if args.strict
+                   else "fast (FMA lerp, within north_star tolerance)",
+                   "l2": "no flush: inputs larger than L2 (2.38 GB stack + 512 MiB volume)",
+                   "parallelism": f"z-slab x{world}" + (" + NCCL slab gather" if world > 1 else ""),
+                   "slab_bounds": [int(b) for b in bounds]},
+        "gpu_launches": total_launches,
+        "visible_updates_per_step": visible_all,
+        "gups_visible": visible_all * args.steps / (ms / 1e3) / 1e9,
         "kernel_ms_per_step": kernel_ms / args.steps,
         "roofline": {"bound": "smem", "achieved": achieved, "peak": peak_nominal,
                      "unit": "GB/s", "frac": achieved / peak_nominal,
-                     "traffic": None,
-                     "peak_source": f"nominal 128 B/clk/SM x 148 SMs at sm_max {sm_max:.0f} MHz",
-                     "frac_at_measured_clock": achieved / (peak_nominal * float(sm_mhz) / float(sm_max))},
+                     "traffic": prof.get("dram_bytes_per_launch"),
+                     "peak_source": f"nominal 128 B/clk/SM x 148 SMs at sm_max {sm_max:.0f} MHz "
+                                    "(MEASURED_PEAKS.json has no shared-memory figure)",
+                     "frac_at_measured_clock": achieved / (peak_nominal * float(sm_mhz) / float(sm_max)),
+                     "fp32_note": "co-limit: FP32 pipe, ~21 lane-ops per update at ~120 lane-ops/clk/SM "
+                                  "measured (DESIGN.md 3.5)"},
         "e2e": {"value": e2e_val, "unit": "GUP/s", "h2d_bytes_per_step": h2d // args.steps,
                 "d2h_bytes_per_step": d2h // args.steps,
-                "ms_per_step": e2e_s * 1e3 / args.steps},
+                "ms_per_step": e2e_s * 1e3 / args.steps,
+                "h2d_ms_per_step": h2d_ms / args.steps, "d2h_ms_per_step": d2h_ms / args.steps},
         "clocks": clocks,
         "tile": {"w": st.tile_w, "h": st.tile_h, "block": [st.block_x, st.block_y, st.block_z],
                  "tile_pairs": st.tile_pairs, "skipped_pairs": st.skipped_pairs,

@@ -239,7 +239,7 @@ void SlabContext::choose_tile(const bpg::BatchArgs& b) {
                 }
     }
     // Row pitch of the SMEM tile == TMA box width.  Pitches == 20 (mod 32) floats
-    // minimise bank conflicts of the 8x4 lane layout (scratch/bank_sim.py).
+    // minimise bank conflicts of the 8x4 lane layout (tools/bank_sim.py).
     int tw = round_up(std::max(need_w, 8) + 4, 4);
     const bool twc_ok = !std::getenv("BP_NO_TWC") && t.stages == 2 &&
                         ((t.bx == 32 && t.bz == 8) || (t.bx == 16 && t.bz == 16));
