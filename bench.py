@@ -285,7 +285,7 @@ def run_ours(args):
 
     # ---- e2e: streamed through the C ABI from pinned host memory ---------------
     e2e_ctx = bp.GpuContext(L, isx, isy, device=device, z_begin=z0, z_end=z1,
-                            strict=args.strict, view_batch=args.batch, ring_batches=3)
+                            strict=args.strict, view_batch=args.batch)
     host_vol = bp.Volume.create(L)  # pinned (library pool); each rank reads back its slab
     out = host_vol.data[z0:z1]
     for _ in range(max(1, args.warmup)):

@@ -422,7 +422,7 @@ class GpuContext:
     """load / backproject / finish / unload (include/bp_gpu.h)."""
 
     def __init__(self, l, isx, isy, *, offset=(0.0, 0.0, 0.0), device=-1, z_begin=0, z_end=0,
-                 view_batch=32, ring_batches=3, strict=True, distance_weight=True,
+                 view_batch=32, ring_batches=0, strict=True, distance_weight=True,
                  row_windows=True, kernel=0, count_visible=False, profile_launches=False,
                  recip_mode=0, device_volume=None):
         cfg = GpuConfig()

@@ -288,7 +288,7 @@ void bp_gpu_config_init(bp_gpu_config* c) {
     std::memset(c, 0, sizeof *c);
     c->device = -1;
     c->view_batch = 32;
-    c->ring_batches = 3;
+    c->ring_batches = 0;  /* library default: 8 batches (tail deferral needs >= 8) */
     c->strict_mode = 1;
     c->distance_weight = 1;
     c->row_windows = 1;

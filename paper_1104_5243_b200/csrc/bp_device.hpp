@@ -46,7 +46,7 @@ enum KernelKind : int { kKernelAuto = 0, kKernelSimple = 1 };
 
 struct TileShape {
     int bx, by, bz;              // voxel block
-    int tw, th;                  // tile capacity (floats), tw % 4 == 0, th % 8 == 0
+    int tw, th;                  // tile pitch (floats, % 4 == 0) and ring rows (% 8 == 0)
     int stages;
     int zp;                      // 1: z-paired thread layout
     int threads;                 // consumer + producer threads per CTA
@@ -70,6 +70,8 @@ int launch_simple(const SlabArgs& s, const BatchArgs& b, bool distance_weight, i
                   void* stream);
 
 int smem_bytes_for(const TileShape& ts);
+// Largest ring (rows) with `ctas` CTAs per SM, at least min_rows.
+int ring_rows_for_shape(const TileShape& ts, int min_rows, int ctas);
 
 // Bitwise check of the kernel's paired reciprocal against __frcp_rn over the
 // float bit patterns [lo_bits, hi_bits).  Synchronous.

@@ -55,7 +55,13 @@ SlabContext::SlabContext(const bp_gpu_config& cfg) : cfg_(cfg) {
     pitch_ = round_up(isx_, 4);  // TMA global strides must be multiples of 16 B
     B_ = cfg.view_batch > 0 ? cfg.view_batch : 32;
     if (B_ > bpg::kMaxBatch) throw bph::config_error("view_batch exceeds 64");
-    R_ = cfg.ring_batches > 0 ? cfg.ring_batches : 3;
+    R_ = cfg.ring_batches > 0 ? cfg.ring_batches : 8;
+    // measured on B200 at 512^3 (tools: scratch e2e A/B): deferring 3 batches and
+    // streaming 8 z-chunks back hides most of the 10 ms volume readback
+    tail_batches_ = std::max(0, std::min(R_ - 2, 3));
+    tail_chunks_ = 8;
+    if (const char* e = std::getenv("BP_TAIL_BATCHES")) tail_batches_ = std::max(0, std::atoi(e));
+    if (const char* e = std::getenv("BP_TAIL_CHUNKS")) tail_chunks_ = std::max(1, std::atoi(e));
     slots_ = B_ * R_;
 
     const size_t vol_elems = (size_t)nz_ * L_ * L_;
@@ -81,6 +87,9 @@ SlabContext::SlabContext(const bp_gpu_config& cfg) : cfg_(cfg) {
     check(cudaMemset(d_cnt_, 0, 8 * sizeof(unsigned long long)), "cudaMemset(counters)");
     check(cudaStreamCreateWithFlags(&s_comp_, cudaStreamNonBlocking), "stream");
     check(cudaStreamCreateWithFlags(&s_copy_, cudaStreamNonBlocking), "stream");
+    check(cudaStreamCreateWithFlags(&s_d2h_, cudaStreamNonBlocking), "stream");
+    ev_chunk_.resize((size_t)tail_chunks_);
+    for (auto& e : ev_chunk_) check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
     ev_ready_.resize((size_t)R_);
     ev_free_.resize((size_t)R_);
     used_.assign((size_t)R_, false);
@@ -98,6 +107,8 @@ SlabContext::~SlabContext() {
     cudaSetDevice(dev_);
     if (s_comp_) cudaStreamSynchronize(s_comp_);
     if (s_copy_) cudaStreamSynchronize(s_copy_);
+    if (s_d2h_) cudaStreamSynchronize(s_d2h_);
+    for (auto e : ev_chunk_) cudaEventDestroy(e);
     for (auto e : ev_ready_) cudaEventDestroy(e);
     for (auto e : ev_free_) cudaEventDestroy(e);
     for (auto& p : launch_ev_) {
@@ -108,6 +119,7 @@ SlabContext::~SlabContext() {
         if (e) cudaEventDestroy(e);
     if (s_comp_) cudaStreamDestroy(s_comp_);
     if (s_copy_) cudaStreamDestroy(s_copy_);
+    if (s_d2h_) cudaStreamDestroy(s_d2h_);
     if (own_vol_ && d_vol_) cudaFree(d_vol_);
     cudaFree(d_ring_);
     cudaFree(d_wx_);
@@ -119,6 +131,8 @@ SlabContext::~SlabContext() {
 }
 
 void SlabContext::reset_recon() {
+    pending_.clear();
+    batch_index_ = 0;
     nb_ = 0;
     any_launch_ = false;
     any_h2d_ = false;
@@ -138,10 +152,14 @@ void SlabContext::backproject(const float* image, const double* A, bool copy) {
     std::memcpy(m.data(), A, sizeof(double) * 12);
     bph::validate_matrix_for_grid(m, grid_);
 
-    if (nb_ == 0 && used_[(size_t)rg_]) {
+    if (nb_ == 0) {
+        // a deferred batch still holding this ring group must be launched first
+        while (std::any_of(pending_.begin(), pending_.end(),
+                           [&](const Pending& p) { return p.rg == rg_; }))
+            launch_pending_front();
         // the ring group (and its pinned staging) is reusable once the kernel
         // that last read it has finished
-        check(cudaEventSynchronize(ev_free_[(size_t)rg_]), "ring wait");
+        if (used_[(size_t)rg_]) check(cudaEventSynchronize(ev_free_[(size_t)rg_]), "ring wait");
     }
     int r0 = 0, r1 = isy_;
     if (cfg_.row_windows)
@@ -241,10 +259,10 @@ void SlabContext::choose_tile(const bpg::BatchArgs& b) {
     // Row pitch of the SMEM tile == TMA box width.  Pitches == 20 (mod 32) floats
     // minimise bank conflicts of the 8x4 lane layout (tools/bank_sim.py).
     int tw = round_up(std::max(need_w, 8) + 4, 4);
-    const bool twc_ok = !std::getenv("BP_NO_TWC") && t.stages == 2 &&
-                        ((t.bx == 32 && t.bz == 8) || (t.bx == 16 && t.bz == 16));
-    if (t.bx == 32 && t.zp && tw <= 144 && twc_ok) tw = 144;
-    if (twc_ok && t.bx == 16 && tw <= 80) {
+    const bool twc_ok = !std::getenv("BP_NO_TWC") &&
+                        ((t.bx == 32 && t.bz == 8) || (t.bx == 16 && t.bz == 16) ||
+                         (t.bx == 32 && t.by == 32 && t.bz == 4));
+    if (twc_ok && t.bx == 16 && t.bz == 16 && tw <= 80) {
         tw = 80;   // compile-time pitch 64+16
     } else if (twc_ok && tw <= 144) {
         tw = 144;  // compile-time pitch 128+16: ALU-only texel addressing, low conflicts
@@ -252,19 +270,20 @@ void SlabContext::choose_tile(const bpg::BatchArgs& b) {
         const int t2 = tw + ((20 - tw % 32) + 32) % 32;
         if (t2 <= 256) tw = t2;
     }
-    int th = round_up(std::max(need_h, 8) + 8, 8);
+    int th = round_up(std::max(need_h, 8) + 8, 8);  // rows of the largest tile (+ guard)
     tw = std::min(tw, 256);
-    th = std::min(th, 256);
     if (tiled_ && tw <= ts_.tw && th <= ts_.th) return;
     if (tiled_) {
         tw = std::max(tw, ts_.tw);
         th = std::max(th, ts_.th);
     }
-    // keep the CTA's dynamic shared memory within the SM budget
+    // The tile rows live in a ring shared by the in-flight views; size it to the
+    // SMEM of `ctas` CTAs per SM (3 for the 288-thread 512^3+ variant).
     t.tw = tw;
-    t.th = th;
-    while (bpg::smem_bytes_for(t) > 220 * 1024 && t.th > 8) t.th -= 8;
+    const int ctas = (t.bx * t.by * t.bz == 4096) ? 3 : 4;
+    t.th = bpg::ring_rows_for_shape(t, th, ctas);
     t.smem_bytes = bpg::smem_bytes_for(t);
+    if (t.smem_bytes > 227 * 1024) throw bph::device_error("tile ring exceeds shared memory");
     char err[256];
     if (bpg::encode_ring_tmap(tmap_, d_ring_, isx_, isy_, pitch_, slots_, t, err, sizeof err) != 0)
         throw bph::device_error(err);
@@ -272,17 +291,18 @@ void SlabContext::choose_tile(const bpg::BatchArgs& b) {
     tiled_ = true;
 }
 
-void SlabContext::launch(const bpg::BatchArgs& b) {
+void SlabContext::launch(const bpg::BatchArgs& b, int zc0, int zc1) {
+    if (zc1 < 0) zc1 = nz_;
     bpg::SlabArgs s{};
-    s.vol = d_vol_;
+    s.vol = d_vol_ + (size_t)zc0 * L_ * L_;
     s.proj = d_ring_;
     s.wx = d_wx_;
     s.wy = d_wy_;
     s.wz = d_wz_;
     s.counters = d_cnt_;
     s.L = L_;
-    s.z0 = z0_;
-    s.nz = nz_;
+    s.z0 = z0_ + zc0;
+    s.nz = zc1 - zc0;
     s.isx = isx_;
     s.isy = isy_;
     s.pitch = pitch_;
@@ -290,7 +310,7 @@ void SlabContext::launch(const bpg::BatchArgs& b) {
     if (tiled_) {
         s.nbx = (L_ + ts_.bx - 1) / ts_.bx;
         s.nby = (L_ + ts_.by - 1) / ts_.by;
-        s.nbz = (nz_ + ts_.bz - 1) / ts_.bz;
+        s.nbz = (s.nz + ts_.bz - 1) / ts_.bz;
     }
     if (cfg_.count_visible) check((cudaError_t)bpg::launch_clip_count(s, b, s_comp_), "clip count");
     cudaEvent_t e0 = nullptr, e1 = nullptr;
@@ -317,34 +337,79 @@ void SlabContext::launch(const bpg::BatchArgs& b) {
     ++launches_;
 }
 
+void SlabContext::launch_pending_front() {
+    Pending p = pending_.front();
+    pending_.erase(pending_.begin());
+    check(cudaStreamWaitEvent(s_comp_, ev_ready_[(size_t)p.rg], 0), "wait");
+    if (!any_launch_) check(cudaEventRecord(ev_t0_, s_comp_), "event");
+    p.b.load_volume = p.index > 0 ? 1 : 0;
+    launch(p.b);
+    any_launch_ = true;
+    check(cudaEventRecord(ev_free_[(size_t)p.rg], s_comp_), "event");
+    used_[(size_t)p.rg] = true;
+}
+
 void SlabContext::flush() {
     if (nb_ == 0) return;
     cur_.nviews = nb_;
-    cur_.load_volume = any_launch_ ? 1 : 0;
     choose_tile(cur_);
     check(cudaEventRecord(ev_ready_[(size_t)rg_], s_copy_), "event");
-    check(cudaStreamWaitEvent(s_comp_, ev_ready_[(size_t)rg_], 0), "wait");
-    if (!any_launch_) check(cudaEventRecord(ev_t0_, s_comp_), "event");
-    launch(cur_);
-    any_launch_ = true;
-    check(cudaEventRecord(ev_free_[(size_t)rg_], s_comp_), "event");
-    used_[(size_t)rg_] = true;
+    pending_.push_back(Pending{cur_, rg_, batch_index_++});
     rg_ = (rg_ + 1) % R_;
     nb_ = 0;
+    while ((int)pending_.size() > tail_batches_) launch_pending_front();
 }
 
 void SlabContext::finish(float* host_volume, bp_gpu_stats* st) {
     bind();
     if (views_ == 0) wall_t0_ = now_ms();
     flush();
-    if (!any_launch_) {
-        check(cudaEventRecord(ev_t0_, s_comp_), "event");
-        check(cudaMemsetAsync(d_vol_, 0, (size_t)nz_ * L_ * L_ * sizeof(float), s_comp_), "memset");
-    }
-    check(cudaEventRecord(ev_t1_, s_comp_), "event");
-    if (any_h2d_) check(cudaEventRecord(ev_h1_, s_copy_), "event");
     const size_t vbytes = (size_t)nz_ * L_ * L_ * sizeof(float);
-    if (host_volume) {
+    bool d2h_done = false;
+    if (host_volume && !pending_.empty() && tiled_ && tail_chunks_ > 1 && nz_ >= 2 * ts_.bz) {
+        // chunk-major tail: for each z-chunk run all deferred batches (ascending
+        // view order per voxel is preserved), then stream that chunk back while the
+        // next chunk computes
+        const int C = std::min(tail_chunks_, nz_ / ts_.bz);
+        std::vector<int> zb((size_t)C + 1);
+        for (int c = 0; c <= C; ++c) zb[(size_t)c] = (int)((long long)nz_ * c / C / ts_.bz) * ts_.bz;
+        zb[(size_t)C] = nz_;
+        for (const auto& p : pending_)
+            check(cudaStreamWaitEvent(s_comp_, ev_ready_[(size_t)p.rg], 0), "wait");
+        if (!any_launch_) check(cudaEventRecord(ev_t0_, s_comp_), "event");
+        for (int c = 0; c < C; ++c) {
+            for (auto p : pending_) {
+                p.b.load_volume = p.index > 0 ? 1 : 0;
+                launch(p.b, zb[(size_t)c], zb[(size_t)c + 1]);
+            }
+            check(cudaEventRecord(ev_chunk_[(size_t)c], s_comp_), "event");
+            check(cudaStreamWaitEvent(s_d2h_, ev_chunk_[(size_t)c], 0), "wait");
+            if (c == 0) check(cudaEventRecord(ev_d0_, s_d2h_), "event");
+            const size_t off = (size_t)zb[(size_t)c] * L_ * L_;
+            const size_t n = (size_t)(zb[(size_t)c + 1] - zb[(size_t)c]) * L_ * L_;
+            check(cudaMemcpyAsync(host_volume + off, d_vol_ + off, n * sizeof(float),
+                                  cudaMemcpyDeviceToHost, s_d2h_),
+                  "D2H");
+        }
+        any_launch_ = true;
+        for (const auto& p : pending_) {
+            check(cudaEventRecord(ev_free_[(size_t)p.rg], s_comp_), "event");
+            used_[(size_t)p.rg] = true;
+        }
+        pending_.clear();
+        check(cudaEventRecord(ev_t1_, s_comp_), "event");
+        check(cudaEventRecord(ev_d1_, s_d2h_), "event");
+        d2h_done = true;
+    } else {
+        while (!pending_.empty()) launch_pending_front();
+        if (!any_launch_) {
+            check(cudaEventRecord(ev_t0_, s_comp_), "event");
+            check(cudaMemsetAsync(d_vol_, 0, vbytes, s_comp_), "memset");
+        }
+        check(cudaEventRecord(ev_t1_, s_comp_), "event");
+    }
+    if (any_h2d_) check(cudaEventRecord(ev_h1_, s_copy_), "event");
+    if (host_volume && !d2h_done) {
         check(cudaEventRecord(ev_d0_, s_comp_), "event");
         check(cudaMemcpyAsync(host_volume, d_vol_, vbytes, cudaMemcpyDeviceToHost, s_comp_), "D2H");
         check(cudaEventRecord(ev_d1_, s_comp_), "event");
@@ -354,6 +419,7 @@ void SlabContext::finish(float* host_volume, bp_gpu_stats* st) {
     check(cudaMemsetAsync(d_cnt_, 0, sizeof cnt, s_comp_), "counters");
     check(cudaStreamSynchronize(s_copy_), "sync");
     check(cudaStreamSynchronize(s_comp_), "sync");
+    check(cudaStreamSynchronize(s_d2h_), "sync");
     if (st) {
         std::memset(st, 0, sizeof *st);
         st->wall_ms = now_ms() - wall_t0_;

@@ -50,9 +50,16 @@ public:
     void bind() const;
 
 private:
+    struct Pending {
+        bpg::BatchArgs b;
+        int rg;          // ring group holding the batch's projections
+        uint64_t index;  // batch index within the reconstruction
+    };
     void flush();
     void choose_tile(const bpg::BatchArgs& b);
-    void launch(const bpg::BatchArgs& b);
+    // launch over slab-local z range [zc0, zc1) (default: the whole slab)
+    void launch(const bpg::BatchArgs& b, int zc0 = 0, int zc1 = -1);
+    void launch_pending_front();
     void reset_recon();
 
     bp_gpu_config cfg_;
@@ -80,6 +87,15 @@ private:
     bool tiled_ = false;
     bpg::TileShape ts_{};
     alignas(64) unsigned char tmap_[128];
+
+    // deferred tail: the last tail_batches_ batches are held back and, when the
+    // volume is read back, processed z-chunk-major so each finished chunk's D2H
+    // overlaps the next chunk's kernels
+    std::vector<Pending> pending_;
+    int tail_batches_ = 3, tail_chunks_ = 8;
+    uint64_t batch_index_ = 0;
+    cudaStream_t s_d2h_ = nullptr;
+    std::vector<cudaEvent_t> ev_chunk_;
 
     // per-reconstruction state
     bpg::BatchArgs cur_{};
