@@ -48,7 +48,6 @@ struct TileShape {
     int bx, by, bz;              // voxel block
     int tw, th;                  // tile pitch (floats, % 4 == 0) and ring rows (% 8 == 0)
     int stages;
-    int zp;                      // 1: z-paired thread layout
     int threads;                 // consumer + producer threads per CTA
     int smem_bytes;
 };

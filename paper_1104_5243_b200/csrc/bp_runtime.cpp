@@ -259,12 +259,8 @@ void SlabContext::choose_tile(const bpg::BatchArgs& b) {
     // Row pitch of the SMEM tile == TMA box width.  Pitches == 20 (mod 32) floats
     // minimise bank conflicts of the 8x4 lane layout (tools/bank_sim.py).
     int tw = round_up(std::max(need_w, 8) + 4, 4);
-    const bool twc_ok = !std::getenv("BP_NO_TWC") &&
-                        ((t.bx == 32 && t.bz == 8) || (t.bx == 16 && t.bz == 16) ||
-                         (t.bx == 32 && t.by == 32 && t.bz == 4));
-    if (twc_ok && t.bx == 16 && t.bz == 16 && tw <= 80) {
-        tw = 80;   // compile-time pitch 64+16
-    } else if (twc_ok && tw <= 144) {
+    const bool twc_ok = !std::getenv("BP_NO_TWC") && t.bx == 32;
+    if (twc_ok && tw <= 144) {
         tw = 144;  // compile-time pitch 128+16: ALU-only texel addressing, low conflicts
     } else if (tw % 32 != 20) {
         const int t2 = tw + ((20 - tw % 32) + 32) % 32;
@@ -280,7 +276,9 @@ void SlabContext::choose_tile(const bpg::BatchArgs& b) {
     // The tile rows live in a ring shared by the in-flight views; size it to the
     // SMEM of `ctas` CTAs per SM (3 for the 288-thread 512^3+ variant).
     t.tw = tw;
-    const int ctas = (t.bx * t.by * t.bz == 4096) ? 3 : 4;
+    int ctas = (t.bx * t.by * t.bz == 4096) ? 3 : 4;
+    if (t.bx == 32 && t.by == 16 && t.bz == 4) ctas = 5;
+    if (t.bx == 32 && t.by == 32 && t.bz == 4) ctas = 2;
     t.th = bpg::ring_rows_for_shape(t, th, ctas);
     t.smem_bytes = bpg::smem_bytes_for(t);
     if (t.smem_bytes > 227 * 1024) throw bph::device_error("tile ring exceeds shared memory");
