@@ -283,6 +283,16 @@ def run_ours(args):
     launches_per_step = launches / args.steps
     ctx.close()
 
+    # strict (bitwise-reference) arithmetic on the same resident data, reported beside
+    strict_ms = None
+    if not args.strict and world == 1:
+        sctx = bp.GpuContext(L, isx, isy, device=device, strict=True, view_batch=args.batch,
+                             ring_batches=ring)
+        sctx.upload_stack(stack)
+        sctx.time_resident(1)
+        strict_ms, _ = sctx.time_resident(args.steps)
+        sctx.close()
+
     # ---- e2e: streamed through the C ABI from pinned host memory ---------------
     e2e_ctx = bp.GpuContext(L, isx, isy, device=device, z_begin=z0, z_end=z1,
                             strict=args.strict, view_batch=args.batch)
@@ -354,6 +364,7 @@ def run_ours(args):
         "visible_updates_per_step": visible_all,
         "gups_visible": visible_all * args.steps / (ms / 1e3) / 1e9,
         "kernel_ms_per_step": kernel_ms / args.steps,
+        "value_strict_bitwise": (nominal_step * args.steps / (strict_ms / 1e3) / 1e9) if strict_ms else None,
         "roofline": {"bound": "smem", "achieved": achieved, "peak": peak_nominal,
                      "unit": "GB/s", "frac": achieved / peak_nominal,
                      "traffic": prof.get("dram_bytes_per_launch"),

@@ -63,3 +63,18 @@ def test_fullsize_strict_bitwise_lines_and_fast_tolerance(stack, L, offset, nlin
     finally:
         strict.close()
         fast.close()
+
+
+def test_config2_256_full_volume_strict_bitwise(stack):
+    # BASELINE config 2 (256^3, 496 views of 1248x960): the whole volume, strict mode,
+    # against the CPU oracle -- bitwise
+    L = 256
+    c = bp.GpuContext(L, 1248, 960, device=0, strict=True)
+    try:
+        c.backproject_stack(stack)
+        got, st = c.finish()
+    finally:
+        c.close()
+    assert st.fallback_pairs == 0 and st.tile_pairs > 0
+    ref, _ = O.reconstruct(stack.pixels, stack.matrices, L)
+    assert bitwise_equal(got, ref)
