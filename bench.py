@@ -214,7 +214,7 @@ def run_ours(args):
 
     # ---- visible updates (clip_stats semantics) for the roofline -------------
     with bp.GpuContext(L, isx, isy, device=device, z_begin=z0, z_end=z1, count_visible=True,
-                       view_batch=args.batch, ring_batches=3) as c:
+                       view_batch=32) as c:
         c.backproject_stack(stack)
         _, vst = c.finish(readback=False)
     visible = int(vst.visible_updates)
@@ -295,7 +295,7 @@ def run_ours(args):
 
     # ---- e2e: streamed through the C ABI from pinned host memory ---------------
     e2e_ctx = bp.GpuContext(L, isx, isy, device=device, z_begin=z0, z_end=z1,
-                            strict=args.strict, view_batch=args.batch)
+                            strict=args.strict, view_batch=args.e2e_batch)
     host_vol = bp.Volume.create(L)  # pinned (library pool); each rank reads back its slab
     out = host_vol.data[z0:z1]
     for _ in range(max(1, args.warmup)):
@@ -354,7 +354,7 @@ def run_ours(args):
         "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {"workload": f"{L}^3 x {n} views of 1248x960 (BASELINE config 3)", "l": L,
-                   "views": n, "view_batch": args.batch,
+                   "views": n, "view_batch": args.batch, "e2e_view_batch": args.e2e_batch,
                    "arithmetic": "strict (bitwise reference)" if args.strict
                    else "fast (FMA lerp, within north_star tolerance)",
                    "l2": "no flush: inputs larger than L2 (2.38 GB stack + 512 MiB volume)",
@@ -399,7 +399,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--l", type=int, default=512)
     ap.add_argument("--views", type=int, default=496)
-    ap.add_argument("--batch", type=int, default=32)
+    ap.add_argument("--batch", type=int, default=64, help="views per launch, resident (value) run")
+    ap.add_argument("--e2e-batch", type=int, default=32, help="views per launch, streamed e2e run")
     ap.add_argument("--seed", type=int, default=20110428)
     ap.add_argument("--strict", action="store_true", help="bitwise reference arithmetic")
     ap.add_argument("--cpu-views", type=int, default=8)
