@@ -231,3 +231,17 @@ def ref_forward_project(ellipsoids, mat, isx, isy):
     if rc != 0:
         raise ValueError(R.ref_last_error().decode())
     return out
+
+
+def ref_clip_table(mats, isx, isy, L, *, offset=(0.0, 0.0, 0.0)):
+    """The reference's build_clip_table ranges (n, L, L, 2) u16 and clip_stats total."""
+    R = ref()
+    mats = np.ascontiguousarray(mats, np.float64).reshape(-1, 12)
+    n = mats.shape[0]
+    ranges = np.zeros((n, L, L, 2), np.uint16)
+    tot = C.c_uint64(0)
+    rc = R.ref_clip_table(_d(mats), n, isx, isy, L, *offset,
+                          ranges.ctypes.data_as(C.POINTER(C.c_uint16)), C.byref(tot))
+    if rc != 0:
+        raise ValueError(R.ref_last_error().decode())
+    return ranges, tot.value

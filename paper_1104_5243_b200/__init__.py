@@ -105,6 +105,7 @@ EXPORTED = [
     "bp_volume_create", "bp_volume_data_mut", "bp_gpu_set_devices", "bp_gpu_device_count",
     "bp_partition_slabs", "bp_slab_row_window", "bp_recon_ex_init", "bp_reconstruct_ex",
     "bp_selftest_rcp", "bp_build_info", "bp_gpu_read_lines", "bp_device_compare",
+    "bp_gpu_clip_table",
 ]
 
 
@@ -171,6 +172,7 @@ def lib():
         "bp_selftest_rcp": (ip, [u32, u32, C.POINTER(C.c_uint64)]),
         "bp_gpu_read_lines": (ip, [vp, C.POINTER(ip), C.POINTER(ip), ip, fp]),
         "bp_device_compare": (ip, [vp, vp, C.c_uint64, dp, dp, dp, C.POINTER(C.c_uint64)]),
+        "bp_gpu_clip_table": (ip, [vp, u32, dp, C.POINTER(C.c_uint16), C.POINTER(C.c_uint64)]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)
@@ -403,6 +405,17 @@ def slab_row_window(matrix, isy, l, z_begin, z_end, offset=(0.0, 0.0, 0.0)):
     _check(lib().bp_slab_row_window(_d(m), isy, l, _d(off), z_begin, z_end, C.byref(r0),
                                     C.byref(r1)))
     return r0.value, r1.value
+
+
+def clip_table(stack: Stack, l: int, offset=(0.0, 0.0, 0.0)):
+    """Exact per-line clip ranges (reference BPCT layout) built on the GPU: (ranges, total)."""
+    isx, isy, n = stack.dims
+    ranges = np.zeros((n, l, l, 2), np.uint16)
+    off = np.asarray(offset, np.float64)
+    tot = C.c_uint64(0)
+    _check(lib().bp_gpu_clip_table(stack._h, l, _d(off),
+                                   ranges.ctypes.data_as(C.POINTER(C.c_uint16)), C.byref(tot)))
+    return ranges, tot.value
 
 
 def set_devices(devs) -> None:

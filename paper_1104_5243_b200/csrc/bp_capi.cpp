@@ -10,6 +10,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstring>
+#include <fstream>
 #include <map>
 #include <memory>
 #include <mutex>
@@ -338,6 +339,24 @@ int bp_gpu_read_lines(bp_gpu_ctx* ctx, const int* ys, const int* zs, int n, floa
     return guarded([&] { ctx->c->read_lines(ys, zs, n, out); });
 }
 
+int bp_gpu_clip_table(const bp_stack* s, uint32_t l, const double offset_mm[3], uint16_t* ranges,
+                      uint64_t* total) {
+    if (!s) return fail(BP_EINVAL, "null argument");
+    return guarded([&] {
+        if (s->s.count() < 1) throw bph::validation_error("empty projection stack");
+        bp_gpu_config c;
+        bp_gpu_config_init(&c);
+        c.l = l;
+        c.isx = (uint32_t)s->s.isx;
+        c.isy = (uint32_t)s->s.isy;
+        for (int i = 0; i < 3; ++i) c.offset_mm[i] = offset_mm ? offset_mm[i] : 0.0;
+        c.view_batch = 1;
+        c.ring_batches = 1;
+        bpr::SlabContext ctx(c);
+        ctx.clip_table(s->s.mats[0].data(), s->s.count(), ranges, total);
+    });
+}
+
 int bp_device_compare(const float* d_a, const float* d_b, uint64_t n, double* max_abs_diff,
                       double* max_abs_ref, double* sum_sq_diff, uint64_t* n_bit_diff) {
     if (!d_a || !d_b) return fail(BP_EINVAL, "null argument");
@@ -552,9 +571,35 @@ int bp_reconstruct(const bp_stack* s, const bp_recon_params* p, bp_volume** out,
         ex.distance_weight = p->distance_weight != 0 ? 1 : 0;
         ex.count_visible = p->clip != 0 ? 1 : 0;
         ex.recip_mode = p->recip_mode;
+        // clip cache (capi.cpp:133-143): read the BPCT table if it exists, else build
+        // it (exactly, on the GPU) and write it.  The GPU clips on the fly; the table
+        // supplies the clip_stats the reference reports.
+        bool have_table = false;
+        uint64_t table_total = 0;
+        if (p->clip && p->clip_cache) {
+            std::ifstream probe(p->clip_cache, std::ios::binary);
+            if (probe.good()) {
+                probe.close();
+                auto t = bph::read_clip_table(p->clip_cache);
+                if (t.L != (int)p->l || t.n_views != s->s.count())
+                    throw bph::validation_error("clip table does not match grid/stack dimensions");
+                table_total = t.total_updates();
+            } else {
+                bph::ClipTable t;
+                t.L = (int)p->l;
+                t.n_views = s->s.count();
+                t.ranges.resize((size_t)2 * t.n_views * p->l * p->l);
+                const int rc = bp_gpu_clip_table(s, p->l, nullptr, t.ranges.data(), &table_total);
+                if (rc != BP_OK) throw bph::device_error(g_last_error);
+                bph::write_clip_table(p->clip_cache, t);
+            }
+            have_table = true;
+            ex.count_visible = 0;
+        }
         bp_gpu_stats gs{};
         const double t0 = bpr::now_ms();
         const int rc = bp_reconstruct_ex(s, p->l, &ex, vol->v.vox.data(), &gs);
+        if (have_table) gs.visible_updates = table_total;
         if (rc != BP_OK) {
             const std::string m = g_last_error;
             if (rc == BP_EINVAL) throw bph::config_error(m);

@@ -80,6 +80,11 @@ int selftest_rcp(uint32_t lo_bits, uint32_t hi_bits, unsigned long long* mismatc
 int device_compare(const float* a, const float* b, unsigned long long n, double* res3,
                    unsigned long long* nbit);
 
+// Reference BPCT clip ranges for views [view0, view0 + b.nviews) of a full-volume
+// table (u16 pairs, precompute.hpp:14-25).
+int launch_clip_ranges(const SlabArgs& s, const BatchArgs& b, uint16_t* ranges, int view0,
+                       void* stream);
+
 // Exact visible-update count (clip_stats semantics, precompute.cpp:93-103)
 // for views [0,n) of the batch: adds into counters[3].
 int launch_clip_count(const SlabArgs& s, const BatchArgs& b, void* stream);

@@ -644,6 +644,39 @@ Volume read_volume(const std::string& path) {
     return v;
 }
 
+uint64_t ClipTable::total_updates() const {
+    uint64_t t = 0;
+    for (size_t i = 0; i + 1 < ranges.size(); i += 2)
+        if (ranges[i] != 0xFFFF) t += (uint64_t)(ranges[i + 1] - ranges[i] + 1);
+    return t;
+}
+
+void write_clip_table(const std::string& path, const ClipTable& t) {
+    std::ofstream f(path, std::ios::binary);
+    if (!f) throw io_error("cannot open " + path + " for writing");
+    f.write("BPCT", 4);
+    put(f, (uint32_t)t.L);
+    put(f, (uint32_t)t.n_views);
+    f.write(reinterpret_cast<const char*>(t.ranges.data()),
+            (std::streamsize)(t.ranges.size() * sizeof(uint16_t)));
+    if (!f) throw io_error("write failed for " + path);
+}
+
+ClipTable read_clip_table(const std::string& path) {
+    std::ifstream f(path, std::ios::binary);
+    if (!f) throw io_error("cannot open " + path);
+    magic(f, "BPCT", path);
+    const uint32_t l = get<uint32_t>(f, "L", path), n = get<uint32_t>(f, "count", path);
+    if (l < 1 || l > 65535 || n < 1) throw io_error("implausible clip table header in " + path, 4);
+    ClipTable t;
+    t.L = (int)l;
+    t.n_views = (int)n;
+    t.ranges.resize((size_t)2 * n * l * l);
+    read_exact(f, reinterpret_cast<char*>(t.ranges.data()),
+               (std::streamsize)(t.ranges.size() * sizeof(uint16_t)), "clip table", path);
+    return t;
+}
+
 double psnr(const float* v, const float* ref, size_t n, double peak) {
     double mse = 0.0;
     for (size_t i = 0; i < n; ++i) {

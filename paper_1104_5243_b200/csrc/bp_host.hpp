@@ -147,6 +147,15 @@ Stack read_stack(const std::string& path);
 void write_volume(const std::string& path, const Volume& v);
 Volume read_volume(const std::string& path);
 
+// BPCT clip cache (precompute.hpp:14-43): "BPCT", u32 L, u32 count, count*L^2 (u16 first, u16 last)
+struct ClipTable {
+    int L = 0, n_views = 0;
+    std::vector<uint16_t> ranges;
+    uint64_t total_updates() const;  // clip_stats (precompute.cpp:93-103)
+};
+void write_clip_table(const std::string& path, const ClipTable& t);
+ClipTable read_clip_table(const std::string& path);
+
 double psnr(const float* v, const float* ref, size_t n, double peak);  // psnr.hpp:14-29
 
 }  // namespace bph

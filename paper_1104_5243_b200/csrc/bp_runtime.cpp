@@ -471,6 +471,50 @@ void SlabContext::read_lines(const int* ys, const int* zs, int n, float* out) {
     check(cudaStreamSynchronize(s_comp_), "sync");
 }
 
+void SlabContext::clip_table(const double* mats, int count, uint16_t* host_ranges,
+                             uint64_t* total) {
+    if (!mats || count < 1) throw bph::config_error("null argument");
+    if (z0_ != 0 || z1_ != L_) throw bph::config_error("clip tables cover the whole grid");
+    if (L_ > 65535) throw bph::config_error("clip table supports at most 65535 voxels per edge");
+    bind();
+    const size_t n = (size_t)2 * count * L_ * L_;
+    uint16_t* d = nullptr;
+    check(cudaMalloc(&d, n * sizeof(uint16_t)), "cudaMalloc(clip table)");
+    bpg::SlabArgs s{};
+    s.wx = d_wx_;
+    s.wy = d_wy_;
+    s.wz = d_wz_;
+    s.counters = d_cnt_;
+    s.L = L_;
+    s.z0 = 0;
+    s.nz = L_;
+    s.isx = isx_;
+    s.isy = isy_;
+    check(cudaMemsetAsync(d_cnt_, 0, 8 * sizeof(unsigned long long), s_comp_), "memset");
+    for (int k0 = 0; k0 < count; k0 += bpg::kMaxBatch) {
+        bpg::BatchArgs b{};
+        b.nviews = std::min(bpg::kMaxBatch, count - k0);
+        for (int i = 0; i < b.nviews; ++i) {
+            bph::Mat m;
+            std::memcpy(m.data(), mats + 12 * (size_t)(k0 + i), sizeof(double) * 12);
+            bph::validate_matrix_for_grid(m, grid_);
+            const auto f = bph::narrowed(m);
+            std::memcpy(b.A[i], f.data(), sizeof(float) * 12);
+        }
+        check((cudaError_t)bpg::launch_clip_ranges(s, b, d, k0, s_comp_), "clip ranges");
+        check((cudaError_t)bpg::launch_clip_count(s, b, s_comp_), "clip count");
+    }
+    unsigned long long cnt[8] = {0};
+    check(cudaMemcpyAsync(cnt, d_cnt_, sizeof cnt, cudaMemcpyDeviceToHost, s_comp_), "counters");
+    if (host_ranges)
+        check(cudaMemcpyAsync(host_ranges, d, n * sizeof(uint16_t), cudaMemcpyDeviceToHost, s_comp_),
+              "D2H clip table");
+    check(cudaMemsetAsync(d_cnt_, 0, sizeof cnt, s_comp_), "memset");
+    check(cudaStreamSynchronize(s_comp_), "sync");
+    cudaFree(d);
+    if (total) *total = cnt[3];
+}
+
 void SlabContext::upload_views(const float* pixels, const double* mats, int count) {
     if (!pixels || !mats) throw bph::config_error("null argument");
     if (count < 1 || count > slots_)

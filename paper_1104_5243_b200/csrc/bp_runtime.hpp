@@ -40,6 +40,8 @@ public:
     void finish(float* host_volume, bp_gpu_stats* st);
     void upload_views(const float* pixels, const double* mats, int count);
     void read_lines(const int* ys, const int* zs, int n, float* out);
+    // exact per-line clip ranges (BPCT layout) for `count` matrices over the whole grid
+    void clip_table(const double* mats, int count, uint16_t* host_ranges, uint64_t* total);
     double time_resident(int iters, bp_gpu_stats* st);
 
     float* device_volume() const { return d_vol_; }

@@ -52,9 +52,12 @@ def main():
     line = O.ref_reconstruct_lines(img, A[None], 256, np.array([130], np.int32),
                                    np.array([136], np.int32))
     save("line_pixel_centre.npz", image=img, mats=A[None], line=line)
-    # 6. clip statistics
+    # 6. clip statistics and the full per-line clip table (build_clip_table)
     tot = O.ref_clip_total(mats, 156, 120, 32)
     save("clip_baseline_32.npz", mats=mats, total=np.array(tot, np.uint64))
+    ranges, tot2 = O.ref_clip_table(mats, 156, 120, 32)
+    assert tot2 == tot
+    save("clip_ranges_baseline_32.npz", mats=mats, ranges=ranges, total=np.array(tot, np.uint64))
 
 
 if __name__ == "__main__":

@@ -270,3 +270,45 @@ def test_approx_recip_modes_match_reference_ladder():
     ap, _ = bp.reconstruct(st, bp.recon_params(16, recip_mode=bp.BP_RECIP_APPROX12))
     p_nr, p_12 = nr.psnr(exact), ap.psnr(exact)
     assert p_nr >= 90.0 and p_12 <= p_nr - 20.0 and p_12 > 20.0
+
+
+# ---- clip table / clip_cache (precompute.cpp:51-134, capi.cpp:133-143) ----------
+
+def test_gpu_clip_table_matches_reference_golden():
+    import os
+    g = np.load(os.path.join(os.path.dirname(__file__), "golden", "clip_ranges_baseline_32.npz"))
+    mats = g["mats"]
+    st = bp.Stack.from_arrays(np.zeros((mats.shape[0], 120, 156), np.float32), mats)
+    ranges, total = bp.clip_table(st, 32)
+    assert np.array_equal(ranges, g["ranges"])
+    assert total == int(g["total"])
+
+
+def test_gpu_clip_table_matches_live_reference():
+    if not O.ref_available():
+        pytest.skip("oracle/_ref not built")
+    px, mats = small_stack("spheres3", 5, 48, 40)
+    st = bp.Stack.from_arrays(px, mats)
+    for L in (20, 33):
+        ranges, total = bp.clip_table(st, L)
+        ref_r, ref_t = O.ref_clip_table(mats, 48, 40, L)
+        assert np.array_equal(ranges, ref_r) and total == ref_t
+
+
+def test_clip_cache_written_then_reused(tmp_path):
+    import os
+    px, mats = baseline_small(n_views=10, shrink=8)
+    st = bp.Stack.from_arrays(px, mats)
+    cache = str(tmp_path / "t.bpct")
+    v1, s1 = bp.reconstruct(st, bp.recon_params(24, clip=1, clip_cache=cache))
+    assert os.path.exists(cache)
+    m1 = os.path.getmtime(cache)
+    v2, s2 = bp.reconstruct(st, bp.recon_params(24, clip=1, clip_cache=cache))
+    assert os.path.getmtime(cache) == m1                 # reused, not rewritten
+    assert bitwise_equal(v1.data, v2.data)
+    assert s1.voxel_updates == s2.voxel_updates == int(O.visible_updates(mats, 156, 120, 24).sum())
+    assert s1.clip_reduction > 0
+    # a table for another grid is rejected (scheduler.cpp:40-42)
+    with pytest.raises(bp.BPError) as e:
+        bp.reconstruct(st, bp.recon_params(16, clip=1, clip_cache=cache))
+    assert e.value.code == bp.BP_EVERIFY
