@@ -323,6 +323,27 @@ def run_ours(args):
     e2e_ctx.close()
     e2e_val = nominal_step * args.steps / e2e_s / 1e9
 
+    # ---- FDK e2e: the same stream with the GPU cosine + ramp
+    # filter applied to every view in the ring before backprojection ----------------
+    fdk = None
+    if world == 1 and not args.no_fdk:
+        geom = (750.0, 1200.0, 0.32 * 1248.0 / isx)
+        fctx = bp.GpuContext(L, isx, isy, device=device, strict=args.strict,
+                             view_batch=args.e2e_batch, filter=geom)
+        for _ in range(max(1, args.warmup)):
+            fctx.backproject_stack(stack)
+            fctx.finish(out=out)
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            fctx.backproject_stack(stack)
+            fctx.finish(out=out)
+        fdk_s = time.perf_counter() - t0
+        fctx.close()
+        fdk = {"value": nominal_step * args.steps / fdk_s / 1e9, "unit": "GUP/s",
+               "ms_per_step": fdk_s * 1e3 / args.steps,
+               "note": "e2e with GPU FDK preprocessing (cosine weight + Ram-Lak FFT filter, "
+                       "bp_filter.cu) of each uploaded view; the reference has no filter"}
+
     # ---- CPU baseline (rank 0, N=1 only) ----------------------------------------
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -383,6 +404,8 @@ def run_ours(args):
                  "fallback_pairs": st.fallback_pairs},
         "datagen_s": gen_s,
     }
+    if fdk:
+        line["fdk_e2e"] = fdk
     if cpu:
         line["cpu_baseline"] = cpu
     print(json.dumps(line), flush=True)
@@ -405,6 +428,7 @@ def main():
     ap.add_argument("--strict", action="store_true", help="bitwise reference arithmetic")
     ap.add_argument("--cpu-views", type=int, default=8)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-fdk", action="store_true", help="skip the e2e run with GPU filtering")
     args = ap.parse_args()
     args.fast_off = args.strict
     if args.impl == "reference":

@@ -61,7 +61,8 @@ class GpuConfig(C.Structure):
                 ("z_end", C.c_int), ("view_batch", C.c_int), ("ring_batches", C.c_int),
                 ("strict_mode", C.c_int), ("distance_weight", C.c_int), ("row_windows", C.c_int),
                 ("kernel", C.c_int), ("count_visible", C.c_int), ("profile_launches", C.c_int),
-                ("recip_mode", C.c_int), ("device_volume", C.c_void_p)]
+                ("recip_mode", C.c_int), ("device_volume", C.c_void_p), ("filter", C.c_int),
+                ("sid_mm", C.c_double), ("sdd_mm", C.c_double), ("pitch_mm", C.c_double)]
 
 
 class GpuStats(C.Structure):
@@ -89,7 +90,8 @@ class ReconEx(C.Structure):
     _fields_ = [("offset_mm", C.POINTER(C.c_double)), ("n_devices", C.c_int),
                 ("virtual_slabs", C.c_int), ("view_batch", C.c_int), ("strict_mode", C.c_int),
                 ("distance_weight", C.c_int), ("kernel", C.c_int), ("row_windows", C.c_int),
-                ("count_visible", C.c_int), ("recip_mode", C.c_int)]
+                ("count_visible", C.c_int), ("recip_mode", C.c_int), ("filter", C.c_int),
+                ("sid_mm", C.c_double), ("sdd_mm", C.c_double), ("pitch_mm", C.c_double)]
 
 
 # Every symbol declared in include/*.h (checked by tests/test_host_abi.py).
@@ -105,7 +107,7 @@ EXPORTED = [
     "bp_volume_create", "bp_volume_data_mut", "bp_gpu_set_devices", "bp_gpu_device_count",
     "bp_partition_slabs", "bp_slab_row_window", "bp_recon_ex_init", "bp_reconstruct_ex",
     "bp_selftest_rcp", "bp_build_info", "bp_gpu_read_lines", "bp_device_compare",
-    "bp_gpu_clip_table",
+    "bp_gpu_clip_table", "bp_gpu_filter_views",
 ]
 
 
@@ -173,6 +175,7 @@ def lib():
         "bp_gpu_read_lines": (ip, [vp, C.POINTER(ip), C.POINTER(ip), ip, fp]),
         "bp_device_compare": (ip, [vp, vp, C.c_uint64, dp, dp, dp, C.POINTER(C.c_uint64)]),
         "bp_gpu_clip_table": (ip, [vp, u32, dp, C.POINTER(C.c_uint16), C.POINTER(C.c_uint64)]),
+        "bp_gpu_filter_views": (ip, [fp, fp, ip, u32, u32, C.c_double, C.c_double, C.c_double, ip]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)
@@ -349,8 +352,11 @@ def reconstruct(stack: Stack, params: ReconParams):
 
 def reconstruct_ex(stack: Stack, l: int, *, offset=(0.0, 0.0, 0.0), n_devices=0,
                    virtual_slabs=0, view_batch=32, strict=True, distance_weight=True, kernel=0,
-                   row_windows=True, count_visible=False, recip_mode=0, out=None):
-    """bp_reconstruct_ex: multi-slab reconstruction into a numpy (L, L, L) array."""
+                   row_windows=True, count_visible=False, recip_mode=0, filter=None, out=None):
+    """bp_reconstruct_ex: multi-slab reconstruction into a numpy (L, L, L) array.
+
+    filter=(sid_mm, sdd_mm, pitch_mm) runs the GPU cosine + ramp filter on every
+    (raw) view before backprojection."""
     p = ReconEx()
     lib().bp_recon_ex_init(C.byref(p))
     off = (C.c_double * 3)(*offset)
@@ -364,6 +370,9 @@ def reconstruct_ex(stack: Stack, l: int, *, offset=(0.0, 0.0, 0.0), n_devices=0,
     p.row_windows = int(row_windows)
     p.count_visible = int(count_visible)
     p.recip_mode = recip_mode
+    if filter is not None:
+        p.filter = 1
+        p.sid_mm, p.sdd_mm, p.pitch_mm = (float(v) for v in filter)
     if out is None:
         out = np.empty((l, l, l), np.float32)
     st = GpuStats()
@@ -418,6 +427,19 @@ def clip_table(stack: Stack, l: int, offset=(0.0, 0.0, 0.0)):
     return ranges, tot.value
 
 
+def filter_views(pixels, sid: float, sdd: float, pitch: float, *, device: int = -1, out=None):
+    """bp_gpu_filter_views: FDK cosine weight + Ram-Lak row filter of (n, isy, isx) images on the GPU."""
+    px = np.ascontiguousarray(pixels, np.float32)
+    if px.ndim == 2:
+        px = px[None]
+    n, isy, isx = px.shape
+    if out is None:
+        out = np.empty_like(px)
+    _check(lib().bp_gpu_filter_views(_f(px), _f(out), n, isx, isy, C.c_double(sid), C.c_double(sdd),
+                                     C.c_double(pitch), device))
+    return out
+
+
 def set_devices(devs) -> None:
     arr = (C.c_int * len(devs))(*devs)
     _check(lib().bp_gpu_set_devices(arr, len(devs)))
@@ -437,7 +459,7 @@ class GpuContext:
     def __init__(self, l, isx, isy, *, offset=(0.0, 0.0, 0.0), device=-1, z_begin=0, z_end=0,
                  view_batch=32, ring_batches=0, strict=True, distance_weight=True,
                  row_windows=True, kernel=0, count_visible=False, profile_launches=False,
-                 recip_mode=0, device_volume=None):
+                 recip_mode=0, device_volume=None, filter=None):
         cfg = GpuConfig()
         lib().bp_gpu_config_init(C.byref(cfg))
         cfg.l, cfg.isx, cfg.isy = l, isx, isy
@@ -451,6 +473,9 @@ class GpuContext:
         cfg.row_windows = int(row_windows)
         cfg.kernel = kernel
         cfg.count_visible = int(count_visible)
+        if filter is not None:  # (sid_mm, sdd_mm, pitch_mm): filter raw views on upload
+            cfg.filter = 1
+            cfg.sid_mm, cfg.sdd_mm, cfg.pitch_mm = (float(v) for v in filter)
         cfg.profile_launches = int(profile_launches)
         cfg.recip_mode = recip_mode
         cfg.device_volume = device_volume

@@ -54,7 +54,7 @@ int guarded(Fn&& fn) {
 // alive between calls so that repeated reconstructions pay neither cudaMalloc
 // of the volume / projection ring nor stream creation.
 using CtxKey = std::tuple<int, uint32_t, uint32_t, uint32_t, double, double, double, int, int, int,
-                          int, int, int, int, int, int>;
+                          int, int, int, int, int, int, int, double, double, double>;
 
 struct CtxCache {
     std::mutex mu;
@@ -69,7 +69,7 @@ CtxKey key_of(const bp_gpu_config& c) {
     return CtxKey{c.device,        c.l,           c.isx,         c.isy,        c.offset_mm[0],
                   c.offset_mm[1],  c.offset_mm[2], c.z_begin,     c.z_end,      c.view_batch,
                   c.strict_mode,   c.distance_weight, c.row_windows, c.kernel, c.count_visible,
-                  c.recip_mode};
+                  c.recip_mode,    c.filter,      c.sid_mm,      c.sdd_mm,     c.pitch_mm};
 }
 
 std::unique_ptr<bpr::SlabContext> acquire(const bp_gpu_config& c) {
@@ -357,6 +357,35 @@ int bp_gpu_clip_table(const bp_stack* s, uint32_t l, const double offset_mm[3], 
     });
 }
 
+int bp_gpu_filter_views(const float* in, float* out, int count, uint32_t isx, uint32_t isy,
+                        double sid_mm, double sdd_mm, double pitch_mm, int device) {
+    if (!in || !out || count < 1) return fail(BP_EINVAL, "null argument");
+    return guarded([&] {
+        if (isx < 2 || isy < 2) throw bph::config_error("detector must be at least 2x2 pixels");
+        int ndev = 0;
+        if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev < 1) {
+            cudaGetLastError();
+            throw bph::device_error("no CUDA device available (the GPU path has no CPU fallback)");
+        }
+        if (device >= ndev) throw bph::config_error("device ordinal out of range");
+        if (device >= 0) bpr::check(cudaSetDevice(device), "cudaSetDevice");
+        bpr::RampFilter f((int)isx, (int)isy, sid_mm, sdd_mm, pitch_mm);
+        const size_t img = (size_t)isx * isy;
+        const int chunk = (int)std::max<size_t>(1, std::min<size_t>((size_t)count, ((size_t)256 << 20) / (img * 4)));
+        float* d = nullptr;
+        bpr::check(cudaMalloc(&d, (size_t)chunk * img * sizeof(float)), "cudaMalloc(filter views)");
+        std::unique_ptr<float, decltype(&cudaFree)> hold(d, &cudaFree);
+        for (int k0 = 0; k0 < count; k0 += chunk) {
+            const int n = std::min(chunk, count - k0);
+            bpr::check(cudaMemcpy(d, in + (size_t)k0 * img, (size_t)n * img * sizeof(float),
+                                  cudaMemcpyHostToDevice), "H2D");
+            f.apply(d, (long long)img, (int)isx, n, 0, (int)isy, nullptr);
+            bpr::check(cudaMemcpy(out + (size_t)k0 * img, d, (size_t)n * img * sizeof(float),
+                                  cudaMemcpyDeviceToHost), "D2H");
+        }
+    });
+}
+
 int bp_device_compare(const float* d_a, const float* d_b, uint64_t n, double* max_abs_diff,
                       double* max_abs_ref, double* sum_sq_diff, uint64_t* n_bit_diff) {
     if (!d_a || !d_b) return fail(BP_EINVAL, "null argument");
@@ -486,6 +515,10 @@ int bp_reconstruct_ex(const bp_stack* s, uint32_t l, const bp_recon_ex* p, float
                     c.kernel = p->kernel;
                     c.count_visible = p->count_visible;
                     c.recip_mode = p->recip_mode;
+                    c.filter = p->filter;
+                    c.sid_mm = p->sid_mm;
+                    c.sdd_mm = p->sdd_mm;
+                    c.pitch_mm = p->pitch_mm;
                     auto ctx = acquire(c);
                     for (int k = 0; k < s->s.count(); ++k)
                         ctx->backproject(s->s.image(k), s->s.mats[(size_t)k].data(), false);

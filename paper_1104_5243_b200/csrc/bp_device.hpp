@@ -8,6 +8,8 @@
 // registers across the batch instead of the reference's per-line linebuf.
 #pragma once
 
+#include <cuda_runtime.h>
+
 #include <cstdint>
 
 namespace bpg {
@@ -88,5 +90,24 @@ int launch_clip_ranges(const SlabArgs& s, const BatchArgs& b, uint16_t* ranges, 
 // Exact visible-update count (clip_stats semantics, precompute.cpp:93-103)
 // for views [0,n) of the batch: adds into counters[3].
 int launch_clip_count(const SlabArgs& s, const BatchArgs& b, void* stream);
+
+// ---- FDK preprocessing: cosine weight + Ram-Lak row filter (bp_filter.cu) ----
+constexpr int kMaxFilterM = 16384;  // FFT length; isx <= 8192
+struct FilterArgs {
+    float* img;             // view y: img + (per_view ? slot[y] : y) * view_stride
+    long long view_stride;  // floats
+    int pitch;              // floats per detector row
+    int isx, row0, row1;    // rows [row0, row1) are filtered in place (per_view == 0)
+    int per_view;           // nonzero: slot / vrow0 / vrow1 per blockIdx.y
+    int slot[kMaxBatch];
+    int vrow0[kMaxBatch], vrow1[kMaxBatch];
+    int M, ngroups;         // FFT length (power of two >= 2*isx); register passes
+    int r[8];               // radix-2 stages per pass, leading pass first (sum = log2 M)
+    int twoff[8];           // pass i: twiddle table at tw + twoff[i], r[i] float2 per j < g_i
+    const float2* tw;       // alpha_{i,j,s} = exp(-2 pi i j / (2 g_i 2^s)), s < r[i]
+    const float* hperm;     // tau/M * H[bitrev(p)]
+    double sdd, cu, cv, pitch_mm;
+};
+int launch_ramp_filter(const FilterArgs& a, int nviews, cudaStream_t stream);
 
 }  // namespace bpg

@@ -500,14 +500,20 @@ void fft(std::vector<std::complex<double>>& a, bool inverse,
 }
 }  // namespace
 
-void cosine_ramp_filter(float* img, int isx, int isy, double sid, double sdd, double pitch) {
-    // FDK preprocessing (PAPER.md:104-108): cosine weight, then a row-wise
-    // Ram-Lak ramp filter applied by zero-padded FFT convolution.
+RampSpectrum ramp_spectrum(int isx, double sid, double sdd, double pitch) {
+    // Ram-Lak kernel sampled at the isocentre pitch tau (Kak & Slaney ch. 3,
+    // eq. 61), zero-padded to M >= 2*isx so the circular convolution is linear
+    // on the isx outputs; h is real and even, so its spectrum is real.
+    if (isx < 2) throw config_error("detector must be at least 2 pixels wide");
+    if (!(sid > 0) || !(sdd > 0) || !(pitch > 0)) throw config_error("filter geometry must be positive");
+    RampSpectrum r;
     size_t M = 1;
     while (M < (size_t)2 * isx) M <<= 1;
+    r.M = (int)M;
+    r.tau = pitch * sid / sdd;  // detector sampling at the isocentre
+    const double tau = r.tau;
     std::vector<std::complex<double>> tw(M / 2);
     for (size_t k = 0; k < M / 2; ++k) tw[k] = std::polar(1.0, -2.0 * M_PI * (double)k / (double)M);
-    const double tau = pitch * sid / sdd;  // detector sampling at the isocentre
     std::vector<std::complex<double>> h(M, 0.0);
     for (long n = -(isx - 1); n <= isx - 1; ++n) {
         double v;
@@ -520,6 +526,18 @@ void cosine_ramp_filter(float* img, int isx, int isy, double sid, double sdd, do
         h[(size_t)((n + (long)M) % (long)M)] = v;
     }
     fft(h, false, tw);
+    r.H.resize(M);
+    for (size_t k = 0; k < M; ++k) r.H[k] = h[k].real();
+    r.tw = std::move(tw);
+    return r;
+}
+
+void cosine_ramp_filter(float* img, int isx, int isy, double sid, double sdd, double pitch) {
+    // FDK preprocessing (PAPER.md:104-108): cosine weight, then a row-wise
+    // Ram-Lak ramp filter applied by zero-padded FFT convolution.
+    const RampSpectrum rs = ramp_spectrum(isx, sid, sdd, pitch);
+    const size_t M = (size_t)rs.M;
+    const double tau = rs.tau;
     const double cu = 0.5 * (isx - 1), cv = 0.5 * (isy - 1);
     // Two real rows per complex FFT: h is real and even, so its spectrum is
     // real and filtering (a + i b) yields (a*h) + i (b*h) exactly.
@@ -533,9 +551,9 @@ void cosine_ramp_filter(float* img, int isx, int isy, double sid, double sdd, do
         for (size_t i = 0; i < M; ++i) row[i] = 0.0;
         for (int iu = 0; iu < isx; ++iu)
             row[(size_t)iu] = std::complex<double>(weighted(iv, iu), pair ? weighted(iv + 1, iu) : 0.0);
-        fft(row, false, tw);
-        for (size_t i = 0; i < M; ++i) row[i] *= h[i].real();
-        fft(row, true, tw);
+        fft(row, false, rs.tw);
+        for (size_t i = 0; i < M; ++i) row[i] *= rs.H[i];
+        fft(row, true, rs.tw);
         float* r0 = img + (size_t)iv * isx;
         for (int iu = 0; iu < isx; ++iu) r0[iu] = static_cast<float>(row[(size_t)iu].real() * tau);
         if (pair) {

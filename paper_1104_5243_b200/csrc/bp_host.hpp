@@ -6,6 +6,7 @@
 #pragma once
 
 #include <array>
+#include <complex>
 #include <cstdint>
 #include <stdexcept>
 #include <string>
@@ -139,7 +140,19 @@ struct BaselineSpec {
 std::vector<Mat> baseline_trajectory(const BaselineSpec& s);
 std::vector<Ellipsoid> baseline_phantom(const BaselineSpec& s);
 Stack make_baseline_stack(const BaselineSpec& s);
+// FDK projection preprocessing: cosine weight sdd / sqrt(sdd^2 + du^2 + dv^2)
+// and a row-wise Ram-Lak ramp filter by zero-padded FFT (double precision).
 void cosine_ramp_filter(float* img, int isx, int isy, double sid, double sdd, double pitch);
+// The ramp filter's frequency response: M = smallest power of two >= 2*isx,
+// tau = pitch*sid/sdd, H[k] = DFT_M(h)[k] (real; h is real and even), and the
+// forward twiddles exp(-2 pi i k / M), k < M/2.
+struct RampSpectrum {
+    int M = 0;
+    double tau = 0.0;
+    std::vector<double> H;
+    std::vector<std::complex<double>> tw;
+};
+RampSpectrum ramp_spectrum(int isx, double sid, double sdd, double pitch);
 
 // ---- file formats (datagen.hpp:49-57, precompute.hpp:41-43) ----------------
 void write_stack(const std::string& path, const Stack& s);

@@ -27,6 +27,107 @@ namespace {
 int round_up(int v, int m) { return (v + m - 1) / m * m; }
 }  // namespace
 
+RampFilter::RampFilter(int isx, int isy, double sid, double sdd, double pitch) {
+    if (isx > bpg::kMaxFilterM / 2) throw bph::config_error("filter: detector wider than 8192 pixels");
+    const bph::RampSpectrum rs = bph::ramp_spectrum(isx, sid, sdd, pitch);
+    const int M = rs.M;
+    int q = 0;
+    while ((1 << q) < M) ++q;
+    // register passes of <= 4 radix-2 stages; the leading pass takes the remainder
+    base_.ngroups = 0;
+    int lead = q % 4 == 0 ? 4 : q % 4;
+    if (q < 4) lead = q;
+    base_.r[base_.ngroups++] = lead;
+    for (int left = q - lead; left > 0; left -= 4) base_.r[base_.ngroups++] = 4;
+    // per-pass twiddle bases alpha_{i,j,s} = exp(-2 pi i j / (2 g_i 2^s)) = W_M^(j M / (2 g_i 2^s)),
+    // taken from the double-precision table (bp_filter.cu twiddle())
+    std::vector<float2> tw;
+    int lg = q;
+    for (int i = 0; i < base_.ngroups; ++i) {
+        lg -= base_.r[i];
+        base_.twoff[i] = (int)tw.size();
+        const int g = 1 << lg;
+        for (int j = 0; j < g; ++j)
+            for (int s = 0; s < base_.r[i]; ++s) {
+                const size_t k = (size_t)j * (size_t)M / ((size_t)2 * g << s);
+                tw.push_back(make_float2((float)rs.tw[k].real(), (float)rs.tw[k].imag()));
+            }
+    }
+    std::vector<float> hp((size_t)M);
+    for (int p = 0; p < M; ++p) {
+        int rev = 0;
+        for (int b = 0; b < q; ++b) rev |= ((p >> b) & 1) << (q - 1 - b);
+        hp[(size_t)p] = (float)(rs.H[(size_t)rev] * rs.tau / (double)M);
+    }
+    check(cudaMalloc(&d_tw_, tw.size() * sizeof(float2)), "cudaMalloc(filter)");
+    check(cudaMalloc(&d_h_, hp.size() * sizeof(float)), "cudaMalloc(filter)");
+    check(cudaMemcpy(d_tw_, tw.data(), tw.size() * sizeof(float2), cudaMemcpyHostToDevice), "filter");
+    check(cudaMemcpy(d_h_, hp.data(), hp.size() * sizeof(float), cudaMemcpyHostToDevice), "filter");
+    base_.isx = isx;
+    base_.M = M;
+    base_.tw = d_tw_;
+    base_.hperm = d_h_;
+    base_.sdd = sdd;
+    base_.cu = 0.5 * (isx - 1);
+    base_.cv = 0.5 * (isy - 1);
+    base_.pitch_mm = pitch;
+}
+
+RampFilter::~RampFilter() {
+    cudaFree(d_tw_);
+    cudaFree(d_h_);
+}
+
+void RampFilter::apply_batch(float* d_ring, long long view_stride, int pitch, int n, const int* slots,
+                             const int* r0s, const int* r1s, cudaStream_t s) const {
+    if (n < 1 || n > bpg::kMaxBatch) throw bph::config_error("filter batch out of range");
+    bpg::FilterArgs a = base_;
+    a.img = d_ring;
+    a.view_stride = view_stride;
+    a.pitch = pitch;
+    a.per_view = 1;
+    int lo = 0, hi = 0;
+    for (int i = 0; i < n; ++i) {
+        a.slot[i] = slots[i];
+        a.vrow0[i] = r0s[i];
+        a.vrow1[i] = r1s[i];
+        hi = std::max(hi, r1s[i] - r0s[i]);
+    }
+    a.row0 = lo;
+    a.row1 = hi;  // grid.x covers the tallest window
+    check((cudaError_t)bpg::launch_ramp_filter(a, n, s), "ramp filter launch");
+}
+
+void RampFilter::apply(float* d_img, long long view_stride, int pitch, int nviews, int r0, int r1,
+                       cudaStream_t s) const {
+    bpg::FilterArgs a = base_;
+    a.img = d_img;
+    a.view_stride = view_stride;
+    a.pitch = pitch;
+    a.row0 = r0;
+    a.row1 = r1;
+    check((cudaError_t)bpg::launch_ramp_filter(a, nviews, s), "ramp filter launch");
+}
+
+void SlabContext::filter_pending(Pending& p) {
+    // FDK preprocessing of a batch's ring slots in place, one launch on the
+    // compute stream right before the batch's first backprojection launch (its
+    // uploads are complete by then), so it neither delays the copy stream nor
+    // stalls earlier, ready backprojection launches behind a pending upload
+    if (!filt_ || p.filtered) return;
+    filt_->apply_batch(d_ring_, (long long)isy_ * pitch_, pitch_, p.b.nviews, p.b.slot, p.fr0.data(),
+                       p.fr1.data(), s_comp_);
+    filtered_views_ += (uint64_t)p.b.nviews;
+    p.filtered = true;
+}
+
+void SlabContext::mark_t0() {
+    if (!t0_rec_) {
+        check(cudaEventRecord(ev_t0_, s_comp_), "event");
+        t0_rec_ = true;
+    }
+}
+
 void SlabContext::bind() const { check(cudaSetDevice(dev_), "cudaSetDevice"); }
 
 SlabContext::SlabContext(const bp_gpu_config& cfg) : cfg_(cfg) {
@@ -100,6 +201,7 @@ SlabContext::SlabContext(const bp_gpu_config& cfg) : cfg_(cfg) {
     for (cudaEvent_t* e : {&ev_t0_, &ev_t1_, &ev_h0_, &ev_h1_, &ev_d0_, &ev_d1_})
         check(cudaEventCreate(e), "event");
     std::memset(tmap_, 0, sizeof tmap_);
+    if (cfg.filter) filt_ = std::make_unique<RampFilter>(isx_, isy_, cfg.sid_mm, cfg.sdd_mm, cfg.pitch_mm);
     reset_recon();
 }
 
@@ -135,6 +237,7 @@ void SlabContext::reset_recon() {
     batch_index_ = 0;
     nb_ = 0;
     any_launch_ = false;
+    t0_rec_ = false;
     any_h2d_ = false;
     views_ = 0;
     launches_ = 0;
@@ -164,6 +267,12 @@ void SlabContext::backproject(const float* image, const double* A, bool copy) {
     int r0 = 0, r1 = isy_;
     if (cfg_.row_windows)
         bph::row_window(m, grid_, 0, L_ - 1, 0, L_ - 1, z0_, z1_ - 1, isy_, &r0, &r1);
+    if (filt_ && r1 > r0) {
+        // the filter packs rows (2i, 2i+1) into one complex FFT; align the window
+        // to that pairing so results do not depend on the window (or stale rows)
+        r0 &= ~1;
+        if (((r1 - r0) & 1) && r1 < isy_) ++r1;
+    }
     const int slot = rg_ * B_ + nb_;
     if (r1 > r0) {
         const float* src = image + (size_t)r0 * isx_;
@@ -190,6 +299,10 @@ void SlabContext::backproject(const float* image, const double* A, bool copy) {
                                     (size_t)(r1 - r0), cudaMemcpyHostToDevice, s_copy_),
                   "H2D");
         h2d_bytes_ += (uint64_t)(r1 - r0) * isx_ * sizeof(float);
+    }
+    if (filt_) {
+        fr0_[(size_t)nb_] = r1 > r0 ? r0 : 0;
+        fr1_[(size_t)nb_] = r1 > r0 ? r1 : 0;
     }
     const auto f = bph::narrowed(m);
     std::memcpy(cur_.A[nb_], f.data(), sizeof(float) * 12);
@@ -339,7 +452,8 @@ void SlabContext::launch_pending_front() {
     Pending p = pending_.front();
     pending_.erase(pending_.begin());
     check(cudaStreamWaitEvent(s_comp_, ev_ready_[(size_t)p.rg], 0), "wait");
-    if (!any_launch_) check(cudaEventRecord(ev_t0_, s_comp_), "event");
+    mark_t0();
+    filter_pending(p);
     p.b.load_volume = p.index > 0 ? 1 : 0;
     launch(p.b);
     any_launch_ = true;
@@ -352,7 +466,7 @@ void SlabContext::flush() {
     cur_.nviews = nb_;
     choose_tile(cur_);
     check(cudaEventRecord(ev_ready_[(size_t)rg_], s_copy_), "event");
-    pending_.push_back(Pending{cur_, rg_, batch_index_++});
+    pending_.push_back(Pending{cur_, rg_, batch_index_++, fr0_, fr1_});
     rg_ = (rg_ + 1) % R_;
     nb_ = 0;
     while ((int)pending_.size() > tail_batches_) launch_pending_front();
@@ -374,7 +488,8 @@ void SlabContext::finish(float* host_volume, bp_gpu_stats* st) {
         zb[(size_t)C] = nz_;
         for (const auto& p : pending_)
             check(cudaStreamWaitEvent(s_comp_, ev_ready_[(size_t)p.rg], 0), "wait");
-        if (!any_launch_) check(cudaEventRecord(ev_t0_, s_comp_), "event");
+        mark_t0();
+        for (auto& p : pending_) filter_pending(p);
         for (int c = 0; c < C; ++c) {
             for (auto p : pending_) {
                 p.b.load_volume = p.index > 0 ? 1 : 0;
@@ -401,7 +516,7 @@ void SlabContext::finish(float* host_volume, bp_gpu_stats* st) {
     } else {
         while (!pending_.empty()) launch_pending_front();
         if (!any_launch_) {
-            check(cudaEventRecord(ev_t0_, s_comp_), "event");
+            mark_t0();
             check(cudaMemsetAsync(d_vol_, 0, vbytes, s_comp_), "memset");
         }
         check(cudaEventRecord(ev_t1_, s_comp_), "event");
@@ -534,6 +649,7 @@ void SlabContext::upload_views(const float* pixels, const double* mats, int coun
                                 s_copy_),
               "H2D");
     }
+    if (filt_) filt_->apply(d_ring_, (long long)isy_ * pitch_, pitch_, count, 0, isy_, s_copy_);
     check(cudaStreamSynchronize(s_copy_), "sync");
     std::fill(used_.begin(), used_.end(), false);
     resident_ = count;

@@ -17,6 +17,7 @@
 
 #include <array>
 #include <cstdint>
+#include <memory>
 #include <vector>
 
 #include "../../include/bp_gpu.h"
@@ -26,6 +27,28 @@
 namespace bpr {
 
 void check(cudaError_t e, const char* what);
+
+// Device-resident FDK preprocessing plan (bp_filter.cu): twiddles and the
+// bit-reversed ramp spectrum for one detector width and geometry.
+class RampFilter {
+public:
+    RampFilter(int isx, int isy, double sid, double sdd, double pitch);  // on the current device
+    ~RampFilter();
+    RampFilter(const RampFilter&) = delete;
+    RampFilter& operator=(const RampFilter&) = delete;
+    // filter rows [r0, r1) of nviews images in place (row pitch and view stride in floats)
+    void apply(float* d_img, long long view_stride, int pitch, int nviews, int r0, int r1,
+               cudaStream_t s) const;
+    // one launch over a ring batch: view i at slot slots[i], rows [r0s[i], r1s[i])
+    void apply_batch(float* d_ring, long long view_stride, int pitch, int n, const int* slots,
+                     const int* r0s, const int* r1s, cudaStream_t s) const;
+    int fft_length() const { return base_.M; }
+
+private:
+    bpg::FilterArgs base_{};
+    float2* d_tw_ = nullptr;
+    float* d_h_ = nullptr;
+};
 
 class SlabContext {
 public:
@@ -56,13 +79,17 @@ private:
         bpg::BatchArgs b;
         int rg;          // ring group holding the batch's projections
         uint64_t index;  // batch index within the reconstruction
+        std::array<int, bpg::kMaxBatch> fr0, fr1;  // rows to filter per view (cfg_.filter)
+        bool filtered = false;
     };
+    void filter_pending(Pending& p);
     void flush();
     void choose_tile(const bpg::BatchArgs& b);
     // launch over slab-local z range [zc0, zc1) (default: the whole slab)
     void launch(const bpg::BatchArgs& b, int zc0 = 0, int zc1 = -1);
     void launch_pending_front();
     void reset_recon();
+    void mark_t0();  // first compute-stream work of a reconstruction
 
     bp_gpu_config cfg_;
     int dev_ = 0;
@@ -85,6 +112,11 @@ private:
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> launch_ev_;
     size_t launch_ev_used_ = 0;
 
+    // optional FDK preprocessing of every uploaded view (cfg_.filter)
+    std::unique_ptr<RampFilter> filt_;
+    uint64_t filtered_views_ = 0;
+    std::array<int, bpg::kMaxBatch> fr0_{}, fr1_{};  // current batch's filtered rows
+
     // tiled kernel
     bool tiled_ = false;
     bpg::TileShape ts_{};
@@ -104,6 +136,7 @@ private:
     int nb_ = 0;
     int rg_ = 0;
     bool any_launch_ = false;
+    bool t0_rec_ = false;
     bool any_h2d_ = false;
     uint64_t views_ = 0, launches_ = 0, h2d_bytes_ = 0;
     double wall_t0_ = 0.0;
