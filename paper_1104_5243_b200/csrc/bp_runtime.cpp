@@ -373,8 +373,9 @@ void SlabContext::choose_tile(const bpg::BatchArgs& b) {
     // minimise bank conflicts of the 8x4 lane layout (tools/bank_sim.py).
     int tw = round_up(std::max(need_w, 8) + 4, 4);
     const bool twc_ok = !std::getenv("BP_NO_TWC") && t.bx == 32;
-    if (twc_ok && tw <= 144) {
-        tw = 144;  // compile-time pitch 128+16: ALU-only texel addressing, low conflicts
+    const int twc = t.by == 32 ? 176 : 144;
+    if (twc_ok && tw <= twc) {
+        tw = twc;  // compile-time pitch (== 16 mod 32): immediate row offsets, low conflicts
     } else if (tw % 32 != 20) {
         const int t2 = tw + ((20 - tw % 32) + 32) % 32;
         if (t2 <= 256) tw = t2;
@@ -391,7 +392,7 @@ void SlabContext::choose_tile(const bpg::BatchArgs& b) {
     t.tw = tw;
     int ctas = (t.bx * t.by * t.bz == 4096) ? 3 : 4;
     if (t.bx == 32 && t.by == 16 && t.bz == 4) ctas = 5;
-    if (t.bx == 32 && t.by == 32 && t.bz == 4) ctas = 2;
+    if (t.bx == 32 && t.by == 32) ctas = 2;
     t.th = bpg::ring_rows_for_shape(t, th, ctas);
     t.smem_bytes = bpg::smem_bytes_for(t);
     if (t.smem_bytes > 227 * 1024) throw bph::device_error("tile ring exceeds shared memory");
