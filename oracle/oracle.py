@@ -87,7 +87,7 @@ def ref():
         ip = C.POINTER(C.c_int)
         d = C.c_double
         i = C.c_int
-        R.ref_reconstruct.argtypes = [fp, dp, i, i, i, i, d, d, d, i, i, i, i, i, i, fp, dp]
+        R.ref_reconstruct.argtypes = [fp, dp, i, i, i, i, d, d, d, i, i, i, i, i, i, i, fp, dp]
         R.ref_reconstruct_lines.argtypes = [fp, dp, i, i, i, i, d, d, d, ip, ip, i, i, fp]
         R.ref_clip_table.argtypes = [dp, i, i, i, i, d, d, d, C.POINTER(C.c_uint16),
                                      C.POINTER(C.c_uint64)]
@@ -175,13 +175,15 @@ def line_update(line, img, A, L, y, z, x0, x1, *, offset=(0.0, 0.0, 0.0), distan
 # ---- reference (oracle/_ref) entry points --------------------------------
 
 def ref_reconstruct(pixels, mats, L, *, offset=(0.0, 0.0, 0.0), threads=1, chunk=1, block_b=1,
-                    lanes=1, clip=False, distance_weight=True):
+                    lanes=1, clip=False, distance_weight=True, recip=0):
+    """bp::reconstruct of the reference; recip = RecipMode (geometry.hpp:39): 0 exact, 1 approx12,
+    2 approx12_nr."""
     R = ref()
     pixels, mats, n, isx, isy = _prep(pixels, mats)
     out = np.zeros((L, L, L), np.float32)
     st = np.zeros(6, np.float64)
     rc = R.ref_reconstruct(_f(pixels), _d(mats), n, isx, isy, L, *offset, threads, chunk, block_b,
-                           lanes, int(clip), int(distance_weight), _f(out), _d(st))
+                           lanes, int(clip), int(distance_weight), int(recip), _f(out), _d(st))
     if rc != 0:
         raise ValueError(R.ref_last_error().decode())
     return out, {"seconds": st[0], "voxel_updates": int(st[1]), "gups": st[2],

@@ -51,7 +51,8 @@ const char* ref_last_error(void) { return g_err.c_str(); }
 // stats_out[0]=seconds, [1]=voxel_updates, [2]=gups, [3]=writeback, [4]=bytes_copied, [5]=clip_reduction
 int ref_reconstruct(const float* pixels, const double* mats, int n, int isx, int isy, int L,
                     double dx, double dy, double dz, int threads, int chunk, int block_b,
-                    int lanes, int clip, int distance_weight, float* out, double* stats_out) {
+                    int lanes, int clip, int distance_weight, int recip, float* out,
+                    double* stats_out) {
     try {
         auto s = wrap(pixels, mats, n, isx, isy);
         auto g = grid_of(L, dx, dy, dz);
@@ -61,6 +62,7 @@ int ref_reconstruct(const float* pixels, const double* mats, int n, int isx, int
         cfg.block_b = block_b;
         cfg.kernel.lanes = lanes;
         cfg.kernel.distance_weight = distance_weight != 0;
+        cfg.kernel.recip = static_cast<bp::RecipMode>(recip);  // geometry.hpp:39
         cfg.clip = clip != 0;
         bp::RunStats st;
         auto vol = bp::reconstruct(s, g, cfg, &st);

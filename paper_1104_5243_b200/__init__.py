@@ -23,6 +23,7 @@ LIB_PATH = os.environ.get("BP_LIB_PATH") or os.path.join(HERE, "libbackproject.s
 
 BP_OK, BP_EINVAL, BP_EIO, BP_EVERIFY, BP_EINTERNAL = 0, 1, 2, 3, 4
 BP_RECIP_EXACT, BP_RECIP_APPROX12, BP_RECIP_APPROX12_NR = 0, 1, 2
+BP_RECIP_HW_APPROX = 3  # GPU-only extension (include/bp_gpu.h)
 BP_EXTRACT_V1_STORE, BP_EXTRACT_V2_SHIFT = 0, 1
 
 

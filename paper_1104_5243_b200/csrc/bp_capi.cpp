@@ -298,7 +298,7 @@ void bp_gpu_config_init(bp_gpu_config* c) {
 int bp_gpu_load(const bp_gpu_config* cfg, bp_gpu_ctx** out) {
     if (!cfg || !out) return fail(BP_EINVAL, "null argument");
     return guarded([&] {
-        if (cfg->recip_mode < BP_RECIP_EXACT || cfg->recip_mode > BP_RECIP_APPROX12_NR)
+        if (cfg->recip_mode < BP_RECIP_EXACT || cfg->recip_mode > BP_RECIP_HW_APPROX)
             throw bph::config_error("recip_mode out of range");
         auto c = std::make_unique<bp_gpu_ctx>();
         c->c = std::make_unique<bpr::SlabContext>(*cfg);

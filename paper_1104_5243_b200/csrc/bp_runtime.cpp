@@ -133,6 +133,8 @@ void SlabContext::bind() const { check(cudaSetDevice(dev_), "cudaSetDevice"); }
 SlabContext::SlabContext(const bp_gpu_config& cfg) : cfg_(cfg) {
     if (cfg.l < 1) throw bph::config_error("grid edge must be >= 1 voxel");
     if (cfg.isx < 2 || cfg.isy < 2) throw bph::config_error("detector must be at least 2x2 pixels");
+    if (cfg.recip_mode < BP_RECIP_EXACT || cfg.recip_mode > BP_RECIP_HW_APPROX)
+        throw bph::config_error("recip_mode out of range");
     int ndev = 0;
     if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev < 1) {
         cudaGetLastError();

@@ -58,6 +58,11 @@ def main():
     ranges, tot2 = O.ref_clip_table(mats, 156, 120, 32)
     assert tot2 == tot
     save("clip_ranges_baseline_32.npz", mats=mats, ranges=ranges, total=np.array(tot, np.uint64))
+    # 7. reciprocal ladder (recip.hpp:14-23): reconstructions in approx12 / approx12_nr
+    px, mats = O.ref_make_stack("spheres3", 6, 64, 48, pitch=0.32 * 1248 / 64)
+    v12, _ = O.ref_reconstruct(px, mats, 16, threads=2, recip=1)
+    vnr, _ = O.ref_reconstruct(px, mats, 16, threads=2, recip=2)
+    save("recon_recip_16.npz", pixels=px, mats=mats, approx12=v12, approx12_nr=vnr)
 
 
 if __name__ == "__main__":

@@ -272,6 +272,28 @@ def test_approx_recip_modes_match_reference_ladder():
     assert p_nr >= 90.0 and p_12 <= p_nr - 20.0 and p_12 > 20.0
 
 
+@pytest.mark.parametrize("mode", [1, 2])
+def test_approx_recip_modes_bitwise_vs_golden(mode):
+    import os
+    g = np.load(os.path.join(os.path.dirname(__file__), "golden", "recon_recip_16.npz"))
+    st = bp.Stack.from_arrays(g["pixels"], g["mats"])
+    got, _ = bp.reconstruct(st, bp.recon_params(16, recip_mode=mode))
+    assert bitwise_equal(got.data, g["approx12" if mode == 1 else "approx12_nr"])
+
+
+@pytest.mark.parametrize("mode", [1, 2])
+def test_approx_recip_modes_bitwise_vs_reference(mode):
+    # recip_approx12 / recip_approx12_nr (recip.hpp:14-23) are restated operation for
+    # operation on the GPU (double frexp / rint / ldexp, then the float Newton step), so
+    # the whole reconstruction is bitwise the reference's bp::reconstruct with that mode
+    if not O.ref_available():
+        pytest.skip("oracle/_ref not built")
+    px, mats = baseline_small(n_views=12, shrink=8)
+    ref, _ = O.ref_reconstruct(px, mats, 32, threads=4, recip=mode)
+    got, _ = bp.reconstruct(bp.Stack.from_arrays(px, mats), bp.recon_params(32, recip_mode=mode))
+    assert bitwise_equal(got.data, ref), err_stats(got.data, ref)
+
+
 # ---- clip table / clip_cache (precompute.cpp:51-134, capi.cpp:133-143) ----------
 
 def test_gpu_clip_table_matches_reference_golden():
