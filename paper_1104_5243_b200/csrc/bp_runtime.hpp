@@ -89,6 +89,7 @@ private:
     void launch(const bpg::BatchArgs& b, int zc0 = 0, int zc1 = -1);
     void launch_pending_front();
     void reset_recon();
+    void issue_run();  // pending coalesced H2D copy
     void mark_t0();  // first compute-stream work of a reconstruction
 
     bp_gpu_config cfg_;
@@ -130,6 +131,11 @@ private:
     uint64_t batch_index_ = 0;
     cudaStream_t s_d2h_ = nullptr;
     std::vector<cudaEvent_t> ev_chunk_;
+
+    // coalesced H2D run [run_src_, +run_bytes_) -> [run_dst_, ...) on s_copy_
+    const char* run_src_ = nullptr;
+    char* run_dst_ = nullptr;
+    size_t run_bytes_ = 0, run_limit_ = (size_t)32 << 20;
 
     // per-reconstruction state
     bpg::BatchArgs cur_{};
