@@ -388,8 +388,8 @@ void SlabContext::choose_tile(const bpg::BatchArgs& b) {
     // Row pitch of the SMEM tile == TMA box width.  Pitches == 20 (mod 32) floats
     // minimise bank conflicts of the 8x4 lane layout (tools/bank_sim.py).
     int tw = round_up(std::max(need_w, 8) + 4, 4);
-    const bool twc_ok = !std::getenv("BP_NO_TWC") && t.bx == 32;
-    const int twc = t.by == 32 ? 176 : 144;
+    const bool twc_ok = !std::getenv("BP_NO_TWC") && t.bx >= 32;
+    const int twc = t.bx == 64 ? 240 : (t.by == 32 ? 176 : 144);
     if (twc_ok && tw <= twc) {
         tw = twc;  // compile-time pitch (== 16 mod 32): immediate row offsets, low conflicts
     } else if (tw % 32 != 20) {
@@ -408,7 +408,7 @@ void SlabContext::choose_tile(const bpg::BatchArgs& b) {
     t.tw = tw;
     int ctas = (t.bx * t.by * t.bz == 4096) ? 3 : 4;
     if (t.bx == 32 && t.by == 16 && t.bz == 4) ctas = 5;
-    if (t.bx == 32 && t.by == 32) ctas = 2;
+    if ((t.bx == 32 && t.by == 32) || t.bx == 64) ctas = 2;
     t.th = bpg::ring_rows_for_shape(t, th, ctas);
     t.smem_bytes = bpg::smem_bytes_for(t);
     if (t.smem_bytes > 227 * 1024) throw bph::device_error("tile ring exceeds shared memory");
