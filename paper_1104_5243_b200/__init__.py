@@ -63,7 +63,8 @@ class GpuConfig(C.Structure):
                 ("strict_mode", C.c_int), ("distance_weight", C.c_int), ("row_windows", C.c_int),
                 ("kernel", C.c_int), ("count_visible", C.c_int), ("profile_launches", C.c_int),
                 ("recip_mode", C.c_int), ("device_volume", C.c_void_p), ("filter", C.c_int),
-                ("sid_mm", C.c_double), ("sdd_mm", C.c_double), ("pitch_mm", C.c_double)]
+                ("sid_mm", C.c_double), ("sdd_mm", C.c_double), ("pitch_mm", C.c_double),
+                ("output_volume", C.c_void_p)]
 
 
 class GpuStats(C.Structure):
@@ -108,7 +109,7 @@ EXPORTED = [
     "bp_volume_create", "bp_volume_data_mut", "bp_gpu_set_devices", "bp_gpu_device_count",
     "bp_partition_slabs", "bp_slab_row_window", "bp_recon_ex_init", "bp_reconstruct_ex",
     "bp_selftest_rcp", "bp_build_info", "bp_gpu_read_lines", "bp_device_compare",
-    "bp_gpu_clip_table", "bp_gpu_filter_views",
+    "bp_gpu_clip_table", "bp_gpu_filter_views", "bp_ipc_handle", "bp_ipc_open", "bp_ipc_close",
 ]
 
 
@@ -177,6 +178,9 @@ def lib():
         "bp_device_compare": (ip, [vp, vp, C.c_uint64, dp, dp, dp, C.POINTER(C.c_uint64)]),
         "bp_gpu_clip_table": (ip, [vp, u32, dp, C.POINTER(C.c_uint16), C.POINTER(C.c_uint64)]),
         "bp_gpu_filter_views": (ip, [fp, fp, ip, u32, u32, C.c_double, C.c_double, C.c_double, ip]),
+        "bp_ipc_handle": (ip, [vp, C.POINTER(C.c_ubyte)]),
+        "bp_ipc_open": (ip, [C.POINTER(C.c_ubyte), pp]),
+        "bp_ipc_close": (ip, [vp]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)
@@ -441,6 +445,25 @@ def filter_views(pixels, sid: float, sdd: float, pitch: float, *, device: int = 
     return out
 
 
+def ipc_handle(device_ptr: int) -> bytes:
+    """bp_ipc_handle: 64-byte CUDA IPC handle of a device allocation of this process."""
+    buf = (C.c_ubyte * 64)()
+    _check(lib().bp_ipc_handle(C.c_void_p(int(device_ptr)), buf))
+    return bytes(buf)
+
+
+def ipc_open(handle: bytes) -> int:
+    """bp_ipc_open: map another process's device allocation; returns the device pointer."""
+    buf = (C.c_ubyte * 64).from_buffer_copy(handle)
+    p = C.c_void_p()
+    _check(lib().bp_ipc_open(buf, C.byref(p)))
+    return int(p.value)
+
+
+def ipc_close(device_ptr: int) -> None:
+    _check(lib().bp_ipc_close(C.c_void_p(int(device_ptr))))
+
+
 def set_devices(devs) -> None:
     arr = (C.c_int * len(devs))(*devs)
     _check(lib().bp_gpu_set_devices(arr, len(devs)))
@@ -460,7 +483,7 @@ class GpuContext:
     def __init__(self, l, isx, isy, *, offset=(0.0, 0.0, 0.0), device=-1, z_begin=0, z_end=0,
                  view_batch=32, ring_batches=0, strict=True, distance_weight=True,
                  row_windows=True, kernel=0, count_visible=False, profile_launches=False,
-                 recip_mode=0, device_volume=None, filter=None):
+                 recip_mode=0, device_volume=None, filter=None, output_volume=None):
         cfg = GpuConfig()
         lib().bp_gpu_config_init(C.byref(cfg))
         cfg.l, cfg.isx, cfg.isy = l, isx, isy
@@ -474,6 +497,8 @@ class GpuContext:
         cfg.row_windows = int(row_windows)
         cfg.kernel = kernel
         cfg.count_visible = int(count_visible)
+        if output_volume is not None:  # device pointer (int): final pass stores here
+            cfg.output_volume = C.c_void_p(int(output_volume))
         if filter is not None:  # (sid_mm, sdd_mm, pitch_mm): filter raw views on upload
             cfg.filter = 1
             cfg.sid_mm, cfg.sdd_mm, cfg.pitch_mm = (float(v) for v in filter)

@@ -386,6 +386,32 @@ int bp_gpu_filter_views(const float* in, float* out, int count, uint32_t isx, ui
     });
 }
 
+int bp_ipc_handle(const void* device_ptr, unsigned char handle[64]) {
+    if (!device_ptr || !handle) return fail(BP_EINVAL, "null argument");
+    return guarded([&] {
+        cudaIpcMemHandle_t h;
+        bpr::check(cudaIpcGetMemHandle(&h, const_cast<void*>(device_ptr)), "cudaIpcGetMemHandle");
+        static_assert(sizeof h == 64, "CUDA IPC handles are 64 bytes");
+        std::memcpy(handle, &h, sizeof h);
+    });
+}
+
+int bp_ipc_open(const unsigned char handle[64], void** device_ptr) {
+    if (!handle || !device_ptr) return fail(BP_EINVAL, "null argument");
+    return guarded([&] {
+        cudaIpcMemHandle_t h;
+        std::memcpy(&h, handle, sizeof h);
+        void* p = nullptr;
+        bpr::check(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle");
+        *device_ptr = p;
+    });
+}
+
+int bp_ipc_close(void* device_ptr) {
+    if (!device_ptr) return fail(BP_EINVAL, "null argument");
+    return guarded([&] { bpr::check(cudaIpcCloseMemHandle(device_ptr), "cudaIpcCloseMemHandle"); });
+}
+
 int bp_device_compare(const float* d_a, const float* d_b, uint64_t n, double* max_abs_diff,
                       double* max_abs_ref, double* sum_sq_diff, uint64_t* n_bit_diff) {
     if (!d_a || !d_b) return fail(BP_EINVAL, "null argument");

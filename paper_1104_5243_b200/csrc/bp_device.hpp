@@ -29,6 +29,8 @@ struct BatchArgs {
 
 struct SlabArgs {
     float* vol;                  // slab volume [nz][L][L], x fastest (kernel.hpp:26-33)
+    float* vol_out;              // final pass only: store the results here instead of vol
+                                 // (same layout; may be a peer GPU's memory over NVLink)
     const float* proj;           // projection ring [slots][isy][pitch]
     const float* wx;             // world x of voxel i, float(offset_x + i*MM) (kernel.cpp:62)
     const float* wy;

@@ -166,6 +166,9 @@ SlabContext::SlabContext(const bp_gpu_config& cfg) : cfg_(cfg) {
     if (const char* e = std::getenv("BP_TAIL_BATCHES")) tail_batches_ = std::max(0, std::atoi(e));
     if (const char* e = std::getenv("BP_TAIL_CHUNKS")) tail_chunks_ = std::max(1, std::atoi(e));
     if (const char* e = std::getenv("BP_H2D_RUN_MB")) run_limit_ = (size_t)std::max(0, std::atoi(e)) << 20;
+    out_vol_ = cfg.output_volume;
+    // the final batch must be launched by finish(), which knows it is the last
+    if (out_vol_) tail_batches_ = std::max(tail_batches_, 1);
     slots_ = B_ * R_;
 
     const size_t vol_elems = (size_t)nz_ * L_ * L_;
@@ -419,10 +422,13 @@ void SlabContext::choose_tile(const bpg::BatchArgs& b) {
     tiled_ = true;
 }
 
-void SlabContext::launch(const bpg::BatchArgs& b, int zc0, int zc1) {
+void SlabContext::launch(const bpg::BatchArgs& b, int zc0, int zc1, bool final_pass) {
     if (zc1 < 0) zc1 = nz_;
     bpg::SlabArgs s{};
     s.vol = d_vol_ + (size_t)zc0 * L_ * L_;
+    // the last batch of a reconstruction stores its results straight into the output
+    // volume when one is configured (fused gather over NVLink / CUDA IPC)
+    s.vol_out = (final_pass && out_vol_) ? out_vol_ + (size_t)zc0 * L_ * L_ : nullptr;
     s.proj = d_ring_;
     s.wx = d_wx_;
     s.wy = d_wy_;
@@ -465,14 +471,14 @@ void SlabContext::launch(const bpg::BatchArgs& b, int zc0, int zc1) {
     ++launches_;
 }
 
-void SlabContext::launch_pending_front() {
+void SlabContext::launch_pending_front(bool final_pass) {
     Pending p = pending_.front();
     pending_.erase(pending_.begin());
     check(cudaStreamWaitEvent(s_comp_, ev_ready_[(size_t)p.rg], 0), "wait");
     mark_t0();
     filter_pending(p);
     p.b.load_volume = p.index > 0 ? 1 : 0;
-    launch(p.b);
+    launch(p.b, 0, -1, final_pass);
     any_launch_ = true;
     check(cudaEventRecord(ev_free_[(size_t)p.rg], s_comp_), "event");
     used_[(size_t)p.rg] = true;
@@ -515,17 +521,18 @@ void SlabContext::finish(float* host_volume, bp_gpu_stats* st) {
         mark_t0();
         for (auto& p : pending_) filter_pending(p);
         for (int c = 0; c < C; ++c) {
-            for (auto p : pending_) {
+            for (size_t i = 0; i < pending_.size(); ++i) {
+                auto p = pending_[i];
                 p.b.load_volume = p.index > 0 ? 1 : 0;
-                launch(p.b, zb[(size_t)c], zb[(size_t)c + 1]);
+                launch(p.b, zb[(size_t)c], zb[(size_t)c + 1], i + 1 == pending_.size());
             }
             check(cudaEventRecord(ev_chunk_[(size_t)c], s_comp_), "event");
             check(cudaStreamWaitEvent(s_d2h_, ev_chunk_[(size_t)c], 0), "wait");
             if (c == 0) check(cudaEventRecord(ev_d0_, s_d2h_), "event");
             const size_t off = (size_t)zb[(size_t)c] * L_ * L_;
             const size_t n = (size_t)(zb[(size_t)c + 1] - zb[(size_t)c]) * L_ * L_;
-            check(cudaMemcpyAsync(host_volume + off, d_vol_ + off, n * sizeof(float),
-                                  cudaMemcpyDeviceToHost, s_d2h_),
+            check(cudaMemcpyAsync(host_volume + off, result() + off, n * sizeof(float),
+                                  cudaMemcpyDefault, s_d2h_),
                   "D2H");
         }
         any_launch_ = true;
@@ -538,17 +545,17 @@ void SlabContext::finish(float* host_volume, bp_gpu_stats* st) {
         check(cudaEventRecord(ev_d1_, s_d2h_), "event");
         d2h_done = true;
     } else {
-        while (!pending_.empty()) launch_pending_front();
+        while (!pending_.empty()) launch_pending_front(pending_.size() == 1);
         if (!any_launch_) {
             mark_t0();
-            check(cudaMemsetAsync(d_vol_, 0, vbytes, s_comp_), "memset");
+            check(cudaMemsetAsync(result(), 0, vbytes, s_comp_), "memset");
         }
         check(cudaEventRecord(ev_t1_, s_comp_), "event");
     }
     if (any_h2d_) check(cudaEventRecord(ev_h1_, s_copy_), "event");
     if (host_volume && !d2h_done) {
         check(cudaEventRecord(ev_d0_, s_comp_), "event");
-        check(cudaMemcpyAsync(host_volume, d_vol_, vbytes, cudaMemcpyDeviceToHost, s_comp_), "D2H");
+        check(cudaMemcpyAsync(host_volume, result(), vbytes, cudaMemcpyDefault, s_comp_), "D2H");
         check(cudaEventRecord(ev_d1_, s_comp_), "event");
     }
     unsigned long long cnt[8] = {0};
@@ -602,7 +609,7 @@ void SlabContext::read_lines(const int* ys, const int* zs, int n, float* out) {
     for (int i = 0; i < n; ++i) {
         if (ys[i] < 0 || ys[i] >= L_ || zs[i] < z0_ || zs[i] >= z1_)
             throw bph::config_error("line outside the slab");
-        const float* src = d_vol_ + ((size_t)(zs[i] - z0_) * L_ + ys[i]) * L_;
+        const float* src = result() + ((size_t)(zs[i] - z0_) * L_ + ys[i]) * L_;
         check(cudaMemcpyAsync(out + (size_t)i * L_, src, (size_t)L_ * sizeof(float),
                               cudaMemcpyDeviceToHost, s_comp_),
               "D2H line");
@@ -696,7 +703,7 @@ double SlabContext::time_resident(int iters, bp_gpu_stats* st) {
                 b.slot[i] = k0 + i;
             }
             choose_tile(b);
-            launch(b);
+            launch(b, 0, -1, k0 + B_ >= resident_);
         }
     }
     check(cudaEventRecord(ev_t1_, s_comp_), "event");

@@ -68,6 +68,8 @@ public:
     double time_resident(int iters, bp_gpu_stats* st);
 
     float* device_volume() const { return d_vol_; }
+    // where the finished volume lives: cfg.output_volume if set, else the slab buffer
+    float* result() const { return out_vol_ ? out_vol_ : d_vol_; }
     int z_begin() const { return z0_; }
     int z_end() const { return z1_; }
     int device() const { return dev_; }
@@ -86,8 +88,8 @@ private:
     void flush();
     void choose_tile(const bpg::BatchArgs& b);
     // launch over slab-local z range [zc0, zc1) (default: the whole slab)
-    void launch(const bpg::BatchArgs& b, int zc0 = 0, int zc1 = -1);
-    void launch_pending_front();
+    void launch(const bpg::BatchArgs& b, int zc0 = 0, int zc1 = -1, bool final_pass = false);
+    void launch_pending_front(bool final_pass = false);
     void reset_recon();
     void issue_run();  // pending coalesced H2D copy
     void mark_t0();  // first compute-stream work of a reconstruction
@@ -99,6 +101,7 @@ private:
     int B_ = 32, R_ = 3, slots_ = 0;
     bool own_vol_ = true;
     float* d_vol_ = nullptr;
+    float* out_vol_ = nullptr;  // optional final-pass destination (may be peer memory)
     float* d_ring_ = nullptr;
     float* d_wx_ = nullptr;
     float* d_wy_ = nullptr;
