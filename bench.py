@@ -422,8 +422,19 @@ def run_ours(args):
                      "peak_source": f"nominal 128 B/clk/SM x 148 SMs at sm_max {sm_max:.0f} MHz "
                                     "(MEASURED_PEAKS.json has no shared-memory figure)",
                      "frac_at_measured_clock": achieved / (peak_nominal * float(sm_mhz) / float(sm_max)),
-                     "fp32_note": "co-limit: FP32 pipe, ~21 lane-ops per update at ~120 lane-ops/clk/SM "
-                                  "measured (DESIGN.md 3.5)"},
+                     "hbm_check": {
+                         "achieved": (prof.get("dram_bytes_per_launch") or 0) / per_launch_s / 1e9
+                         if prof.get("dram_bytes_per_launch") else None,
+                         "peak": peaks.get("hbm_gbs"), "unit": "GB/s",
+                         "note": "ncu DRAM bytes of one 32-view launch / live mean launch time: HBM is "
+                                 "not the bound (measured copy peak from MEASURED_PEAKS.json)"},
+                     "binding_unit": {
+                         "unit": "LSU shared-memory wavefronts (1 per clk per SM)",
+                         "util": prof.get("lsu_wavefronts_pct", 0.0) / 100.0,
+                         "fma_pipe_util": prof.get("fma_pipe_active_pct", 0.0) / 100.0,
+                         "source": "ncu --set full of the same kernel (profiles/latest.json): 0.236 "
+                                   "wavefronts per computed update, of which 0.071 are bank-conflict "
+                                   "replays (DESIGN.md 3.5)"}},
         "e2e": {"value": e2e_val, "unit": "GUP/s", "h2d_bytes_per_step": h2d // args.steps,
                 "d2h_bytes_per_step": d2h // args.steps,
                 "ms_per_step": e2e_s * 1e3 / args.steps,
