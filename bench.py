@@ -423,11 +423,12 @@ def run_ours(args):
                                     "(MEASURED_PEAKS.json has no shared-memory figure)",
                      "frac_at_measured_clock": achieved / (peak_nominal * float(sm_mhz) / float(sm_max)),
                      "hbm_check": {
-                         "achieved": (prof.get("dram_bytes_per_launch") or 0) / per_launch_s / 1e9
-                         if prof.get("dram_bytes_per_launch") else None,
+                         "achieved": (8.0 * (z1 - z0) * L * L + 4.0 * isx * isy * n / max(1e-9, launches_per_step))
+                         / per_launch_s / 1e9,
                          "peak": peaks.get("hbm_gbs"), "unit": "GB/s",
-                         "note": "ncu DRAM bytes of one 32-view launch / live mean launch time: HBM is "
-                                 "not the bound (measured copy peak from MEASURED_PEAKS.json)"},
+                         "note": "algorithmic HBM bytes per launch (slab volume read + write, the launch's "
+                                 "views) / live mean launch time; ncu agrees (profiles/latest.json). HBM is "
+                                 "not the bound"},
                      "binding_unit": {
                          "unit": "LSU shared-memory wavefronts (1 per clk per SM)",
                          "util": prof.get("lsu_wavefronts_pct", 0.0) / 100.0,
