@@ -392,7 +392,8 @@ void SlabContext::choose_tile(const bpg::BatchArgs& b) {
     // minimise bank conflicts of the 8x4 lane layout (tools/bank_sim.py).
     int tw = round_up(std::max(need_w, 8) + 4, 4);
     const bool twc_ok = !std::getenv("BP_NO_TWC") && t.bx >= 32;
-    const int twc = t.bx == 64 ? 240 : (t.by == 32 ? 176 : 144);
+    int twc = t.bx == 64 ? 240 : (t.by == 32 ? 176 : 144);
+    if (const char* e = std::getenv("BP_TWC")) twc = std::atoi(e);
     if (twc_ok && tw <= twc) {
         tw = twc;  // compile-time pitch (== 16 mod 32): immediate row offsets, low conflicts
     } else if (tw % 32 != 20) {
