@@ -107,12 +107,33 @@ __device__ __forceinline__ void dif_stages(float2 (&e)[R], const float2 (&alpha)
         dif_stages<R, MID, T / 2>(e, alpha);
     }
 }
-// r radix-2 DIT stages with conjugate twiddles, halves g .. g*R/2
-template <int R, bool MID, int T = 1>
+// r radix-2 DIT stages with conjugate twiddles, halves g .. g*R/2 (stages T < TEND)
+template <int R, bool MID, int T = 1, int TEND = R>
 __device__ __forceinline__ void dit_stages(float2 (&e)[R], const float2 (&alpha)[4]) {
-    if constexpr (T < R) {
+    if constexpr (T < TEND) {
         dit_pairs<R, MID, T, 0>(e, alpha);
-        dit_stages<R, MID, T * 2>(e, alpha);
+        dit_stages<R, MID, T * 2, TEND>(e, alpha);
+    }
+}
+
+// Pruned first forward stage: in the pass that reads the rows from HBM, tuple
+// elements m >= R/2 sit at p >= M/2 >= isx and are zero, so the largest-half
+// butterflies reduce to e[m + R/2] = e[m] * w.
+template <int R, int M0 = 0>
+__device__ __forceinline__ void dif_first_pruned(float2 (&e)[R], const float2 (&alpha)[4]) {
+    if constexpr (M0 < R / 2) {
+        e[M0 + R / 2] = cmul(e[M0], twiddle<false, R / 2, M0>(alpha));
+        dif_first_pruned<R, M0 + 1>(e, alpha);
+    }
+}
+// Pruned last inverse stage: only outputs p < M/2 (m < R/2) are ever stored.
+template <int R, int M0 = 0>
+__device__ __forceinline__ void dit_last_pruned(float2 (&e)[R], const float2 (&alpha)[4]) {
+    if constexpr (M0 < R / 2) {
+        constexpr int T = R / 2;
+        const float2 c = cmulc(e[M0 + T], twiddle<false, T, M0>(alpha));
+        e[M0] = cadd(e[M0], c);
+        dit_last_pruned<R, M0 + 1>(e, alpha);
     }
 }
 
@@ -139,11 +160,15 @@ struct RowPair {
 };
 
 // One grouped pass over all tuples.  KIND: 0 forward (DIF), 1 fused middle
-// (DIF, * H, DIT; g == 1), 2 inverse (DIT).
-template <int R, int KIND>
-__device__ void pass(const FilterArgs& a, float2* x, const RowPair& rp, int lg, const float2* tw,
-                     bool from_global, bool to_global) {
+// (DIF, * H, DIT; g == 1), 2 inverse (DIT).  FG: the pass reads the rows from HBM
+// (first forward pass); TG: it writes them back (last inverse pass).
+template <int R, int KIND, bool FG, bool TG>
+__device__ void pass(const FilterArgs& a, float2* x, const RowPair& rp, int lg, const float2* tw) {
     constexpr int r = R == 2 ? 1 : R == 4 ? 2 : R == 8 ? 3 : 4;
+    // pruning applies when the pass spans the whole row (g * R == M): only then are
+    // tuple elements m >= R/2 exactly the positions p >= M/2
+    constexpr bool kPruneIn = FG && KIND == 0 && R >= 2;
+    constexpr bool kPruneOut = TG && KIND == 2 && R >= 2;
     const int g = 1 << lg;
     const int ntup = a.M >> r;
     for (int t = threadIdx.x; t < ntup; t += blockDim.x) {
@@ -158,9 +183,19 @@ __device__ void pass(const FilterArgs& a, float2* x, const RowPair& rp, int lg, 
 #pragma unroll
         for (int m = 0; m < R; ++m) {
             const int p = b + j + m * g;
-            e[m] = from_global ? rp.load(p) : x[swz(p)];
+            if (kPruneIn)
+                e[m] = m < R / 2 ? rp.load(p) : make_float2(0.f, 0.f);
+            else
+                e[m] = FG ? rp.load(p) : x[swz(p)];
         }
-        if constexpr (KIND == 0) dif_stages<R, false>(e, alpha);
+        if constexpr (KIND == 0) {
+            if constexpr (kPruneIn) {
+                dif_first_pruned<R>(e, alpha);
+                dif_stages<R, false, R / 4>(e, alpha);
+            } else {
+                dif_stages<R, false>(e, alpha);
+            }
+        }
         if constexpr (KIND == 1) {
             dif_stages<R, true>(e, alpha);
 #pragma unroll
@@ -171,26 +206,34 @@ __device__ void pass(const FilterArgs& a, float2* x, const RowPair& rp, int lg, 
             }
             dit_stages<R, true>(e, alpha);
         }
-        if constexpr (KIND == 2) dit_stages<R, false>(e, alpha);
+        if constexpr (KIND == 2) {
+            if constexpr (kPruneOut) {
+                dit_stages<R, false, 1, R / 2>(e, alpha);
+                dit_last_pruned<R>(e, alpha);
+            } else {
+                dit_stages<R, false>(e, alpha);
+            }
+        }
 #pragma unroll
         for (int m = 0; m < R; ++m) {
             const int p = b + j + m * g;
-            if (to_global)
-                rp.store(p, e[m]);
-            else
+            if (TG) {
+                if (!kPruneOut || m < R / 2) rp.store(p, e[m]);
+            } else {
                 x[swz(p)] = e[m];
+            }
         }
     }
 }
 
-template <int KIND>
+template <int KIND, bool FG, bool TG>
 __device__ void run_pass(int r, const FilterArgs& a, float2* x, const RowPair& rp, int lg,
-                         const float2* tw, bool from_global, bool to_global) {
+                         const float2* tw) {
     switch (r) {
-        case 1: pass<2, KIND>(a, x, rp, lg, tw, from_global, to_global); break;
-        case 2: pass<4, KIND>(a, x, rp, lg, tw, from_global, to_global); break;
-        case 3: pass<8, KIND>(a, x, rp, lg, tw, from_global, to_global); break;
-        default: pass<16, KIND>(a, x, rp, lg, tw, from_global, to_global); break;
+        case 1: pass<2, KIND, FG, TG>(a, x, rp, lg, tw); break;
+        case 2: pass<4, KIND, FG, TG>(a, x, rp, lg, tw); break;
+        case 3: pass<8, KIND, FG, TG>(a, x, rp, lg, tw); break;
+        default: pass<16, KIND, FG, TG>(a, x, rp, lg, tw); break;
     }
 }
 
@@ -218,20 +261,29 @@ __global__ void __launch_bounds__(256) bp_ramp_filter_kernel(const __grid_consta
     while ((1 << lm) < a.M) ++lm;
     // forward passes; g_i = M >> (r_0 + ... + r_i); the last one (g = 1) is fused
     // with the H multiply and the first inverse pass
-    int lg = lm;
-    for (int gi = 0; gi < ng - 1; ++gi) {
+    if (ng == 1) {  // M <= 16: one pass from HBM to HBM
+        run_pass<1, true, true>(a.r[0], a, fx, rp, 0, nullptr);
+        return;
+    }
+    int lg = lm - a.r[0];
+    run_pass<0, true, false>(a.r[0], a, fx, rp, lg, a.tw + a.twoff[0]);
+    __syncthreads();
+    for (int gi = 1; gi < ng - 1; ++gi) {
         lg -= a.r[gi];
-        run_pass<0>(a.r[gi], a, fx, rp, lg, a.tw + a.twoff[gi], gi == 0, false);
+        run_pass<0, false, false>(a.r[gi], a, fx, rp, lg, a.tw + a.twoff[gi]);
         __syncthreads();
     }
-    run_pass<1>(a.r[ng - 1], a, fx, rp, 0, nullptr, ng == 1, ng == 1);
+    run_pass<1, false, false>(a.r[ng - 1], a, fx, rp, 0, nullptr);
     // remaining inverse passes, g growing back to M >> r_0
     lg = 0;
-    for (int gi = ng - 2; gi >= 0; --gi) {
+    for (int gi = ng - 2; gi >= 1; --gi) {
         __syncthreads();
         lg += a.r[gi + 1];
-        run_pass<2>(a.r[gi], a, fx, rp, lg, a.tw + a.twoff[gi], false, gi == 0);
+        run_pass<2, false, false>(a.r[gi], a, fx, rp, lg, a.tw + a.twoff[gi]);
     }
+    __syncthreads();
+    lg += a.r[1];
+    run_pass<2, false, true>(a.r[0], a, fx, rp, lg, a.tw + a.twoff[0]);
 }
 
 }  // namespace
