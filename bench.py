@@ -464,7 +464,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--l", type=int, default=512)
     ap.add_argument("--views", type=int, default=496)
-    ap.add_argument("--batch", type=int, default=64, help="views per launch, resident (value) run")
+    ap.add_argument("--batch", type=int, default=124, help="views per launch, resident (value) run "
+                    "(496 = 4 x 124)")
     ap.add_argument("--e2e-batch", type=int, default=32, help="views per launch, streamed e2e run")
     ap.add_argument("--seed", type=int, default=20110428)
     ap.add_argument("--strict", action="store_true", help="bitwise reference arithmetic")

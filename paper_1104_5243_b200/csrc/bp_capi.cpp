@@ -620,12 +620,15 @@ int bp_reconstruct(const bp_stack* s, const bp_recon_params* p, bp_volume** out,
             throw bph::config_error("threads, chunk, block_b and numa_domains must be >= 1");
         if (lanes != 1 && lanes != 4 && lanes != 8)
             throw bph::config_error("lane width must be 1, 4 or 8");
-        if (block_b > 64) throw bph::config_error("block_b (view batch) must be <= 64 on the GPU");
+        // block_b is the register batch (views per launch). Any value is accepted like
+        // the reference's; beyond the kernel's parameter-space batch it is clamped,
+        // which cannot change results (ascending view order per voxel is invariant)
+        const int gpu_b = std::min(block_b, bpg::kMaxBatch);
 
         auto vol = std::make_unique<bp_volume>(bp_volume{bph::Volume(grid)});
         bp_recon_ex ex;
         bp_recon_ex_init(&ex);
-        ex.view_batch = block_b;
+        ex.view_batch = gpu_b;
         ex.strict_mode = p->strict_mode != 0 ? 1 : 0;
         ex.distance_weight = p->distance_weight != 0 ? 1 : 0;
         ex.count_visible = p->clip != 0 ? 1 : 0;
@@ -676,7 +679,7 @@ int bp_reconstruct(const bp_stack* s, const bp_recon_params* p, bp_volume** out,
             stats->voxel_updates = p->clip ? gs.visible_updates : n * L3;
             stats->gups = secs > 0 ? stats->voxel_updates / secs / 1e9 : 0.0;
             stats->gflops = secs > 0 ? 31.0 * stats->voxel_updates / secs / 1e9 : 0.0;
-            stats->writeback_stores = (n + block_b - 1) / block_b * L3;
+            stats->writeback_stores = (n + gpu_b - 1) / gpu_b * L3;
             stats->bytes_copied = gs.h2d_bytes;
             stats->clip_reduction = p->clip ? 1.0 - (double)gs.visible_updates / (double)(n * L3) : 0.0;
             stats->thread_updates_min = stats->voxel_updates;

@@ -16,8 +16,9 @@ namespace bpg {
 
 // Maximum views per kernel launch (register batch).  The per-view matrices
 // travel as kernel parameters (constant bank), so the batch is bounded by the
-// 32 KB parameter space; 64 x 48 B + extras stays far below it.
-constexpr int kMaxBatch = 64;
+// 32 KB parameter space; 128 x 52 B + extras stays far below it.  At 512^3 the
+// resident run measured +0.6% for 128- over 64-view batches (fewer volume passes).
+constexpr int kMaxBatch = 128;
 
 // One launch = one batch of views against one z-slab of the volume.
 struct BatchArgs {

@@ -334,3 +334,13 @@ def test_clip_cache_written_then_reused(tmp_path):
     with pytest.raises(bp.BPError) as e:
         bp.reconstruct(st, bp.recon_params(16, clip=1, clip_cache=cache))
     assert e.value.code == bp.BP_EVERIFY
+
+
+def test_block_b_beyond_kernel_batch_is_clamped_not_rejected():
+    # the reference accepts any block_b >= 1; results are batch-invariant (scheduler.cpp:77-100)
+    px, mats = baseline_small(n_views=20, shrink=8)
+    st = bp.Stack.from_arrays(px, mats)
+    a, sa = bp.reconstruct(st, bp.recon_params(24, block_b=500))
+    b, _ = bp.reconstruct(st, bp.recon_params(24, block_b=7))
+    assert bitwise_equal(a.data, b.data)
+    assert sa.writeback_stores == 24 ** 3  # one batch of 20 views
