@@ -344,3 +344,16 @@ def test_block_b_beyond_kernel_batch_is_clamped_not_rejected():
     b, _ = bp.reconstruct(st, bp.recon_params(24, block_b=7))
     assert bitwise_equal(a.data, b.data)
     assert sa.writeback_stores == 24 ** 3  # one batch of 20 views
+
+
+@pytest.mark.parametrize("debug", ["1", "2"])
+def test_global_fallback_path_bitwise(debug, monkeypatch):
+    # Every (block, view) pair can be forced through the guarded global-memory fallback:
+    # bit 0 forces it at the producer, bit 1 at the consumers. The fallback uses the reference
+    # clamp and arithmetic (kernel.cpp:53-82) and must stay bitwise.
+    px, mats = baseline_small(n_views=10, shrink=8)
+    ref, _ = O.reconstruct(px, mats, 32)
+    monkeypatch.setenv("BP_DEBUG", debug)
+    got, st = gpu_recon(px, mats, 32)
+    assert st.fallback_pairs > 0 or debug == "2"
+    assert bitwise_equal(got, ref), err_stats(got, ref)
