@@ -178,7 +178,7 @@ def lib():
         "bp_device_compare": (ip, [vp, vp, C.c_uint64, dp, dp, dp, C.POINTER(C.c_uint64)]),
         "bp_gpu_clip_table": (ip, [vp, u32, dp, C.POINTER(C.c_uint16), C.POINTER(C.c_uint64)]),
         "bp_gpu_filter_views": (ip, [fp, fp, ip, u32, u32, C.c_double, C.c_double, C.c_double, ip]),
-        "bp_ipc_handle": (ip, [vp, C.POINTER(C.c_ubyte)]),
+        "bp_ipc_handle": (ip, [vp, C.POINTER(C.c_ubyte), C.POINTER(C.c_uint64)]),
         "bp_ipc_open": (ip, [C.POINTER(C.c_ubyte), pp]),
         "bp_ipc_close": (ip, [vp]),
     }
@@ -446,22 +446,31 @@ def filter_views(pixels, sid: float, sdd: float, pitch: float, *, device: int = 
 
 
 def ipc_handle(device_ptr: int) -> bytes:
-    """bp_ipc_handle: 64-byte CUDA IPC handle of a device allocation of this process."""
+    """bp_ipc_handle: a 72-byte token for a device pointer of this process. The token is the 64-byte CUDA
+    IPC handle of its allocation plus the pointer's offset inside that allocation."""
     buf = (C.c_ubyte * 64)()
-    _check(lib().bp_ipc_handle(C.c_void_p(int(device_ptr)), buf))
-    return bytes(buf)
+    off = C.c_uint64(0)
+    _check(lib().bp_ipc_handle(C.c_void_p(int(device_ptr)), buf, C.byref(off)))
+    return bytes(buf) + int(off.value).to_bytes(8, "little")
 
 
-def ipc_open(handle: bytes) -> int:
-    """bp_ipc_open: map another process's device allocation; returns the device pointer."""
-    buf = (C.c_ubyte * 64).from_buffer_copy(handle)
+def ipc_open(token: bytes) -> int:
+    """bp_ipc_open: map the allocation behind an ipc_handle() token from another process and return the
+    exporter's pointer in this process. Pass the same value to ipc_close()."""
+    buf = (C.c_ubyte * 64).from_buffer_copy(token[:64])
+    off = int.from_bytes(token[64:72], "little") if len(token) >= 72 else 0
     p = C.c_void_p()
     _check(lib().bp_ipc_open(buf, C.byref(p)))
-    return int(p.value)
+    _ipc_bases[int(p.value) + off] = int(p.value)
+    return int(p.value) + off
+
+
+_ipc_bases = {}
 
 
 def ipc_close(device_ptr: int) -> None:
-    _check(lib().bp_ipc_close(C.c_void_p(int(device_ptr))))
+    base = _ipc_bases.pop(int(device_ptr), int(device_ptr))
+    _check(lib().bp_ipc_close(C.c_void_p(base)))
 
 
 def set_devices(devs) -> None:

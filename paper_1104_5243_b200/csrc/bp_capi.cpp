@@ -5,6 +5,7 @@
 // ABI; config_error -> BP_EINVAL, io_error -> BP_EIO, validation_error ->
 // BP_EVERIFY, everything else (CUDA failures included) -> BP_EINTERNAL, with a
 // thread-local message in bp_last_error().
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -386,13 +387,31 @@ int bp_gpu_filter_views(const float* in, float* out, int count, uint32_t isx, ui
     });
 }
 
-int bp_ipc_handle(const void* device_ptr, unsigned char handle[64]) {
+int bp_ipc_handle(const void* device_ptr, unsigned char handle[64], uint64_t* offset) {
     if (!device_ptr || !handle) return fail(BP_EINVAL, "null argument");
     return guarded([&] {
+        // IPC maps whole allocations: report where device_ptr sits inside its allocation
+        // (a caching allocator may hand out sub-ranges), via cuMemGetAddressRange
+        using RangeFn = CUresult (*)(CUdeviceptr*, size_t*, CUdeviceptr);
+        static RangeFn range = nullptr;
+        if (!range) {
+            void* fp = nullptr;
+            cudaDriverEntryPointQueryResult q;
+            if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &fp, cudaEnableDefault, &q) !=
+                    cudaSuccess ||
+                q != cudaDriverEntryPointSuccess)
+                throw bph::device_error("cuMemGetAddressRange entry point unavailable");
+            range = reinterpret_cast<RangeFn>(fp);
+        }
+        CUdeviceptr base = 0;
+        size_t size = 0;
+        if (range(&base, &size, reinterpret_cast<CUdeviceptr>(device_ptr)) != CUDA_SUCCESS)
+            throw bph::device_error("cuMemGetAddressRange failed (not a device allocation?)");
         cudaIpcMemHandle_t h;
-        bpr::check(cudaIpcGetMemHandle(&h, const_cast<void*>(device_ptr)), "cudaIpcGetMemHandle");
+        bpr::check(cudaIpcGetMemHandle(&h, reinterpret_cast<void*>(base)), "cudaIpcGetMemHandle");
         static_assert(sizeof h == 64, "CUDA IPC handles are 64 bytes");
         std::memcpy(handle, &h, sizeof h);
+        if (offset) *offset = (uint64_t)(reinterpret_cast<CUdeviceptr>(device_ptr) - base);
     });
 }
 

@@ -73,9 +73,13 @@ def test_ipc_fused_gather_across_processes(tmp_path):
     ref, _ = O.reconstruct(px, mats, L)
     path = str(tmp_path / "stack.npz")
     np.savez(path, pixels=px, mats=mats)
+    # a small allocation first, so that `full` sits at a nonzero offset inside the caching
+    # allocator's segment (IPC maps whole allocations; the token carries the offset)
+    pad = torch.zeros(1000, dtype=torch.float32, device="cuda")
     full = torch.full((L, L, L), float("nan"), dtype=torch.float32, device="cuda")
     torch.cuda.synchronize()
     handle = bp.ipc_handle(full.data_ptr())
+    assert int.from_bytes(handle[64:], "little") > 0
     bounds = bp.partition_slabs(mats, isx, isy, L, 2)
     z0, z1 = int(bounds[0]), int(bounds[1])
     # the other "rank": a separate process maps this process's volume and writes slab 1
@@ -93,3 +97,4 @@ def test_ipc_fused_gather_across_processes(tmp_path):
         ctx.finish(readback=False)
     torch.cuda.synchronize()
     assert bitwise_equal(full.cpu().numpy(), ref)
+    assert not pad.any()  # nothing landed outside the slab ranges
