@@ -357,3 +357,19 @@ def test_global_fallback_path_bitwise(debug, monkeypatch):
     got, st = gpu_recon(px, mats, 32)
     assert st.fallback_pairs > 0 or debug == "2"
     assert bitwise_equal(got, ref), err_stats(got, ref)
+
+
+@pytest.mark.parametrize("seed", list(range(8)))
+def test_strict_bitwise_random_geometry_fuzz(seed):
+    # random single-view geometries (test_support.hpp:32-45) stacked into one scan, random
+    # grid offsets and edge lengths (odd L takes the simple kernel): strict mode stays bitwise
+    rng = np.random.default_rng(1000 + seed)
+    isx, isy = int(rng.integers(24, 200)), int(rng.integers(24, 160))
+    n = int(rng.integers(1, 9))
+    mats = np.stack([random_matrix(int(rng.integers(0, 1 << 30)), isx, isy) for _ in range(n)])
+    px = np.stack([random_image(isx, isy, int(rng.integers(0, 1 << 30)), -1.0, 2.0) for _ in range(n)])
+    L = int(rng.choice([16, 31, 48, 64, 96]))
+    off = tuple(float(v) for v in rng.uniform(-40, 40, size=3))
+    ref, _ = O.reconstruct(px, mats, L, offset=off)
+    got, _ = gpu_recon(px, mats, L, offset=off, view_batch=int(rng.integers(1, 9)))
+    assert bitwise_equal(got, ref), err_stats(got, ref)
