@@ -67,7 +67,7 @@ int encode_ring_tmap(void* tmap128, const float* ring, int isx, int isy, int pit
                      const TileShape& ts, char* err, int errlen);
 
 int launch_tiled(const void* tmap128, const SlabArgs& s, const BatchArgs& b,
-                 const TileShape& ts, bool strict, bool distance_weight, void* stream);
+                 const TileShape& ts, bool strict, bool distance_weight, bool hw_rcp, void* stream);
 
 // recip: 0 exact (recip.hpp:12), 1 approx12 (recip.hpp:14-18), 2 approx12_nr (recip.hpp:20-23)
 int launch_simple(const SlabArgs& s, const BatchArgs& b, bool distance_weight, int recip,

@@ -332,7 +332,11 @@ void SlabContext::backproject(const float* image, const double* A, bool copy) {
 }
 
 void SlabContext::choose_tile(const bpg::BatchArgs& b) {
-    if (cfg_.kernel == bpg::kKernelSimple || cfg_.recip_mode != 0) {
+    // the reference's approximate reciprocals (and the strict HW approximation) run on
+    // the simple kernel; fast mode + BP_RECIP_HW_APPROX has a tiled variant
+    const bool tiled_recip = cfg_.recip_mode == BP_RECIP_EXACT ||
+                             (cfg_.recip_mode == BP_RECIP_HW_APPROX && !cfg_.strict_mode);
+    if (cfg_.kernel == bpg::kKernelSimple || !tiled_recip) {
         tiled_ = false;
         return;
     }
@@ -464,7 +468,7 @@ void SlabContext::launch(const bpg::BatchArgs& b, int zc0, int zc1, bool final_p
     int rc;
     if (tiled_)
         rc = bpg::launch_tiled(tmap_, s, b, ts_, cfg_.strict_mode != 0, cfg_.distance_weight != 0,
-                               s_comp_);
+                               cfg_.recip_mode == BP_RECIP_HW_APPROX, s_comp_);
     else
         rc = bpg::launch_simple(s, b, cfg_.distance_weight != 0, cfg_.recip_mode, s_comp_);
     check((cudaError_t)rc, "backprojection kernel launch");

@@ -373,3 +373,18 @@ def test_strict_bitwise_random_geometry_fuzz(seed):
     ref, _ = O.reconstruct(px, mats, L, offset=off)
     got, _ = gpu_recon(px, mats, L, offset=off, view_batch=int(rng.integers(1, 9)))
     assert bitwise_equal(got, ref), err_stats(got, ref)
+
+
+def test_hw_rcp_tiled_fast_mode_within_tolerance():
+    # the opt-in BP_RECIP_HW_APPROX tier on the tiled kernel stays inside the north_star bounds
+    px, mats = baseline_small(n_views=48, shrink=2)
+    ref, _ = O.reconstruct(px, mats, 128)
+    n, isy, isx = px.shape
+    with bp.GpuContext(128, isx, isy, strict=False, recip_mode=bp.BP_RECIP_HW_APPROX) as ctx:
+        for k in range(n):
+            ctx.backproject(px[k], mats[k])
+        got, st = ctx.finish()
+    assert st.tile_pairs > 0  # tiled, not the simple kernel
+    emax, erms = err_stats(got, ref)
+    assert emax <= TOL_MAX and erms <= TOL_RMS, (emax, erms)
+    assert erms > 0  # it is an approximation

@@ -35,6 +35,8 @@ peak = float(np.abs(exact).max())
 rows = [("exact 1/w, strict (== reference bitwise)", exact, t_exact)]
 fast, t = run(strict=False)
 rows.append(("exact 1/w, fast mode (FMA-lerp bilinear)", fast, t))
+v, t = run(strict=False, recip_mode=bp.BP_RECIP_HW_APPROX)
+rows.append(("hardware rcp.approx, fast mode (tiled kernel)", v, t))
 for mode, name in ((bp.BP_RECIP_APPROX12_NR, "approx12_nr (recip.hpp:20-23)"),
                    (bp.BP_RECIP_APPROX12, "approx12 (recip.hpp:14-18)"),
                    (bp.BP_RECIP_HW_APPROX, "hardware rcp.approx.ftz.f32 (GPU only)")):
