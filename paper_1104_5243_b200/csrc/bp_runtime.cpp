@@ -417,6 +417,8 @@ void SlabContext::choose_tile(const bpg::BatchArgs& b) {
     int ctas = (t.bx * t.by * t.bz == 4096) ? 3 : 4;
     if (t.bx == 32 && t.by == 16 && t.bz == 4) ctas = 5;
     if ((t.bx == 32 && t.by == 32) || t.bx == 64) ctas = 2;
+    if (t.bx == 16 && t.by == 32) ctas = 4;
+    if (const char* e = std::getenv("BP_CTAS")) ctas = std::max(1, std::atoi(e));
     t.th = bpg::ring_rows_for_shape(t, th, ctas);
     t.smem_bytes = bpg::smem_bytes_for(t);
     if (t.smem_bytes > 227 * 1024) throw bph::device_error("tile ring exceeds shared memory");
