@@ -396,10 +396,22 @@ void SlabContext::choose_tile(const bpg::BatchArgs& b) {
     // minimise bank conflicts of the 8x4 lane layout (tools/bank_sim.py).
     int tw = round_up(std::max(need_w, 8) + 4, 4);
     const bool twc_ok = !std::getenv("BP_NO_TWC") && t.bx >= 32;
-    int twc = t.bx == 64 ? 240 : (t.by == 32 ? 176 : 144);
+    // compile-time pitches (== 16 mod 32: immediate row offsets, low conflicts); the
+    // smallest listed one that holds the footprint
+    int twcs[3] = {0, 0, 0};
+    if (t.bx == 64) {
+        twcs[0] = 240;
+    } else if (t.by == 32) {
+        twcs[0] = 176;  // narrower 112 at 1024^3 measured 0.9% slower (A/B)
+    } else {
+        twcs[0] = 144;
+    }
+    int twc = 0;
+    for (int c : twcs)
+        if (c > 0 && tw <= c) { twc = c; break; }
     if (const char* e = std::getenv("BP_TWC")) twc = std::atoi(e);
-    if (twc_ok && tw <= twc) {
-        tw = twc;  // compile-time pitch (== 16 mod 32): immediate row offsets, low conflicts
+    if (twc_ok && twc > 0 && tw <= twc) {
+        tw = twc;
     } else if (tw % 32 != 20) {
         const int t2 = tw + ((20 - tw % 32) + 32) % 32;
         if (t2 <= 256) tw = t2;
