@@ -612,6 +612,12 @@ int bp_reconstruct_ex(const bp_stack* s, uint32_t l, const bp_recon_ex* p, float
                 t.block_y = x.block_y;
                 t.block_z = x.block_z;
             }
+            std::vector<uint64_t> dev((size_t)D, 0);
+            for (int g = 0; g < G; ++g)
+                dev[(size_t)(g % D)] += p->count_visible ? per[(size_t)g].visible_updates
+                                                         : per[(size_t)g].nominal_updates;
+            t.device_updates_min = *std::min_element(dev.begin(), dev.end());
+            t.device_updates_max = *std::max_element(dev.begin(), dev.end());
             *stats = t;
         }
     });
@@ -701,8 +707,12 @@ int bp_reconstruct(const bp_stack* s, const bp_recon_params* p, bp_volume** out,
             stats->writeback_stores = (n + gpu_b - 1) / gpu_b * L3;
             stats->bytes_copied = gs.h2d_bytes;
             stats->clip_reduction = p->clip ? 1.0 - (double)gs.visible_updates / (double)(n * L3) : 0.0;
-            stats->thread_updates_min = stats->voxel_updates;
-            stats->thread_updates_max = stats->voxel_updates;
+            // per-device split of the updates, the GPU analogue of the reference's
+            // per-thread min/max (scheduler.hpp:22-30); a cached clip table gives only
+            // the total, so the split is then unknown and the total is reported
+            const bool split = !(p->clip && have_table);
+            stats->thread_updates_min = split ? gs.device_updates_min : stats->voxel_updates;
+            stats->thread_updates_max = split ? gs.device_updates_max : stats->voxel_updates;
         }
     });
 }

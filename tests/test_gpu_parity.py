@@ -388,3 +388,16 @@ def test_hw_rcp_tiled_fast_mode_within_tolerance():
     emax, erms = err_stats(got, ref)
     assert emax <= TOL_MAX and erms <= TOL_RMS, (emax, erms)
     assert erms > 0  # it is an approximation
+
+
+def test_recon_stats_per_device_split():
+    # RunStats' per-thread min/max (scheduler.hpp:22-30) become per-device min/max; with
+    # one device both equal the total, with virtual slabs on one device likewise
+    px, mats = baseline_small(n_views=8, shrink=8)
+    st = bp.Stack.from_arrays(px, mats)
+    _, rs = bp.reconstruct(st, bp.recon_params(32, clip=1))
+    assert rs.thread_updates_min == rs.thread_updates_max == rs.voxel_updates
+    _, rs0 = bp.reconstruct(st, bp.recon_params(32, clip=0))
+    assert rs0.thread_updates_min == rs0.thread_updates_max == rs0.voxel_updates == 8 * 32 ** 3
+    out, gs = bp.reconstruct_ex(st, 32, virtual_slabs=3, count_visible=True)
+    assert gs.device_updates_min == gs.device_updates_max == gs.visible_updates
