@@ -189,11 +189,20 @@ def run_ours(args):
     import paper_1104_5243_b200 as bp
     rank, world, local = dist_env()
     dist = torch = None
+    ctrl = "cuda"  # device of the control-plane tensors (max-reduce of timings etc.)
     if world > 1:
         import torch
         import torch.distributed as dist  # plumbing: barrier, max-reduce, slab gather
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        torch.cuda.set_device(local % torch.cuda.device_count())
+        # BP_BENCH_BACKEND=gloo runs the control plane on CPU tensors: it lets the
+        # multi-rank flow (slabs, row windows, fused IPC gather) be exercised with
+        # several ranks on ONE GPU -- correctness only, never a scaling number
+        backend = os.environ.get("BP_BENCH_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", torch.cuda.current_device()))
+        else:
+            dist.init_process_group(backend)
+            ctrl = "cpu"
     n_dev = bp.device_count()
     if n_dev < 1:
         print(json.dumps({"metric": METRIC, "error": "no CUDA device"}))
@@ -239,7 +248,7 @@ def run_ours(args):
             ok = 1
         except Exception:
             ok = 0
-        flag = torch.tensor([ok], dtype=torch.int32, device="cuda")
+        flag = torch.tensor([ok], dtype=torch.int32, device=ctrl)
         dist.all_reduce(flag, op=dist.ReduceOp.MIN)
         fused = int(flag.item()) == 1
         if fused:
@@ -291,10 +300,10 @@ def run_ours(args):
         kernel_ms += float(st.kernel_ms)
     clocks = clk.stop()
     if dist:
-        t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+        t = torch.tensor([ms], dtype=torch.float64, device=ctrl)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
-        t = torch.tensor([launches], dtype=torch.float64, device="cuda")
+        t = torch.tensor([launches], dtype=torch.float64, device=ctrl)
         dist.all_reduce(t, op=dist.ReduceOp.SUM)
         total_launches = int(t.item())
     else:
@@ -304,11 +313,24 @@ def run_ours(args):
     per_launch_s = kernel_ms / 1e3 / max(1, launches)
     launches_per_step = launches / args.steps
     ctx.close()
+    gather_check = None
     if world > 1:
         torch.cuda.synchronize()
         dist.barrier()  # all final-pass stores into rank 0's volume have landed
         if fused and rank != 0:
             bp.ipc_close(base)
+        if args.verify_gather and rank == 0:
+            # the gathered volume must equal a single-context reconstruction bitwise
+            # (per-voxel arithmetic and view order do not depend on the slab split)
+            one = torch.empty((L, L, L), dtype=torch.float32, device="cuda")
+            vc = bp.GpuContext(L, isx, isy, device=device, strict=args.strict, view_batch=args.batch,
+                               ring_batches=ring, device_volume=one.data_ptr())
+            vc.upload_stack(stack)
+            vc.time_resident(1)
+            vc.close()
+            torch.cuda.synchronize()
+            gather_check = bool(torch.equal(one.view(torch.int32), full_t.view(torch.int32)))
+            del one
 
     # strict (bitwise-reference) arithmetic on the same resident data, reported beside,
     # and the opt-in hardware-reciprocal tier (BP_RECIP_HW_APPROX) for the trade-off
@@ -349,7 +371,7 @@ def run_ours(args):
         d2h_ms += est.d2h_ms
     e2e_s = time.perf_counter() - t0
     if dist:
-        t = torch.tensor([e2e_s, h2d, d2h], dtype=torch.float64, device="cuda")
+        t = torch.tensor([e2e_s, h2d, d2h], dtype=torch.float64, device=ctrl)
         mx = t.clone()
         dist.all_reduce(mx, op=dist.ReduceOp.MAX)
         dist.all_reduce(t, op=dist.ReduceOp.SUM)
@@ -388,7 +410,7 @@ def run_ours(args):
                          f"(bp::reconstruct lanes=8 block_b=8 clip=1; wall {r['wall_s']:.2f} s)"}
 
     if dist:
-        vt = torch.tensor([visible], dtype=torch.float64, device="cuda")
+        vt = torch.tensor([visible], dtype=torch.float64, device=ctrl)
         dist.all_reduce(vt, op=dist.ReduceOp.SUM)
         visible_all = int(vt.item())
     else:
@@ -458,6 +480,8 @@ def run_ours(args):
     }
     if fdk:
         line["fdk_e2e"] = fdk
+    if gather_check is not None:
+        line["gather_bitwise_vs_single_context"] = gather_check
     if cpu:
         line["cpu_baseline"] = cpu
     print(json.dumps(line), flush=True)
@@ -472,7 +496,8 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--l", type=int, default=512)
+    ap.add_argument("--l", "--edge", dest="l", type=int, default=512,
+                    help="voxels per edge (use --edge under torchrun: its parser claims --l)")
     ap.add_argument("--views", type=int, default=496)
     ap.add_argument("--batch", type=int, default=124, help="views per launch, resident (value) run "
                     "(496 = 4 x 124)")
@@ -482,6 +507,8 @@ def main():
     ap.add_argument("--cpu-views", type=int, default=8)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-fdk", action="store_true", help="skip the e2e run with GPU filtering")
+    ap.add_argument("--verify-gather", action="store_true",
+                    help="N>1: compare rank 0's gathered volume with a single-context run")
     args = ap.parse_args()
     args.fast_off = args.strict
     if args.impl == "reference":
