@@ -401,3 +401,22 @@ def test_recon_stats_per_device_split():
     assert rs0.thread_updates_min == rs0.thread_updates_max == rs0.voxel_updates == 8 * 32 ** 3
     out, gs = bp.reconstruct_ex(st, 32, virtual_slabs=3, count_visible=True)
     assert gs.device_updates_min == gs.device_updates_max == gs.visible_updates
+
+
+def test_multi_device_threads_on_one_gpu():
+    # bp_gpu_set_devices([0, 0]): two host worker threads drive two slab contexts
+    # concurrently (bp_reconstruct_ex, one thread per listed device); independent kernels
+    px, mats = baseline_small(n_views=20, shrink=4)
+    stack = bp.Stack.from_arrays(px, mats)
+    ref, _ = O.reconstruct(px, mats, 64)
+    try:
+        bp.set_devices([0, 0])
+        got, st = bp.reconstruct_ex(stack, 64, count_visible=True)
+        assert bitwise_equal(got, ref)
+        assert st.device_updates_min <= st.device_updates_max
+        assert st.device_updates_min + st.device_updates_max == st.visible_updates
+        vol, rs = bp.reconstruct(stack, bp.recon_params(64, clip=1))
+        assert bitwise_equal(vol.data, ref)
+        assert rs.thread_updates_min + rs.thread_updates_max == rs.voxel_updates
+    finally:
+        bp.set_devices([0])
