@@ -108,8 +108,11 @@ struct FilterArgs {
     int r[8];               // radix-2 stages per pass, leading pass first (sum = log2 M)
     int twoff[8];           // pass i: twiddle table at tw + twoff[i], r[i] float2 per j < g_i
     const float2* tw;       // alpha_{i,j,s} = exp(-2 pi i j / (2 g_i 2^s)), s < r[i]
-    const float* hperm;     // tau/M * H[bitrev(p)]
+    const float* hperm;     // tau/M * H[sigma(p)], sigma = the forward network's output order
     double sdd, cu, cv, pitch_mm;
+    // mixed radix: M = R0 * N2 (R0 in {3, 5}, N2 = 2^q); R0 == 1: pure radix-2 (N2 = M)
+    int R0, N2;
+    const float2* twr;      // W_M^(j m') for m' in [1, R0), j < N2: twr[(m'-1) N2 + j]
 };
 int launch_ramp_filter(const FilterArgs& a, int nviews, cudaStream_t stream);
 

@@ -237,6 +237,74 @@ __device__ void run_pass(int r, const FilterArgs& a, float2* x, const RowPair& r
     }
 }
 
+// ---- leading radix-3 / radix-5 pass of a mixed-radix length M = R0 * N2 ----------
+// Forward (DIF): for j < N2, y[m'] = W_M^(j m') * sum_m x[j + m N2] W_R0^(m m'), stored at
+// m' N2 + j; the N2-point radix-2 passes then run inside each of the R0 blocks, so the
+// spectrum lands at sigma(m' N2 + j) = m' + R0 * bitrev(j).  Inverse (DIT): the radix-2
+// passes first, then x[j + m N2] = sum_m' W_R0^(-m m') W_M^(-j m') y_m'[j].
+template <int R0, bool INV>
+__device__ __forceinline__ void dft_small(float2 (&e)[R0]) {
+    // conj(W) for the inverse: swap the sign of the "i" rotations
+    auto rot = [](float2 b, bool plus) {  // plus: +i*b, else -i*b
+        return plus ? make_float2(-b.y, b.x) : make_float2(b.y, -b.x);
+    };
+    if constexpr (R0 == 3) {
+        constexpr float c = -0.5f, sn = 0.866025403784438647f;  // cos, sin(2 pi / 3)
+        const float2 t1 = cadd(e[1], e[2]), t2 = csub(e[1], e[2]);
+        const float2 y0 = cadd(e[0], t1);
+        const float2 a = make_float2(fmaf(c, t1.x, e[0].x), fmaf(c, t1.y, e[0].y));
+        const float2 bb = make_float2(sn * t2.x, sn * t2.y);
+        e[0] = y0;
+        e[1] = cadd(a, rot(bb, INV));
+        e[2] = cadd(a, rot(bb, !INV));
+    } else {
+        constexpr float c1 = 0.309016994374947424f, c2 = -0.809016994374947424f;
+        constexpr float s1 = 0.951056516295153572f, s2 = 0.587785252292473129f;
+        const float2 t1 = cadd(e[1], e[4]), t2 = cadd(e[2], e[3]);
+        const float2 t3 = csub(e[1], e[4]), t4 = csub(e[2], e[3]);
+        const float2 y0 = cadd(e[0], cadd(t1, t2));
+        const float2 a1 = make_float2(fmaf(c1, t1.x, fmaf(c2, t2.x, e[0].x)),
+                                      fmaf(c1, t1.y, fmaf(c2, t2.y, e[0].y)));
+        const float2 a2 = make_float2(fmaf(c2, t1.x, fmaf(c1, t2.x, e[0].x)),
+                                      fmaf(c2, t1.y, fmaf(c1, t2.y, e[0].y)));
+        const float2 b1 = make_float2(fmaf(s1, t3.x, s2 * t4.x), fmaf(s1, t3.y, s2 * t4.y));
+        const float2 b2 = make_float2(fmaf(s2, t3.x, -s1 * t4.x), fmaf(s2, t3.y, -s1 * t4.y));
+        e[0] = y0;
+        e[1] = cadd(a1, rot(b1, INV));
+        e[4] = cadd(a1, rot(b1, !INV));
+        e[2] = cadd(a2, rot(b2, INV));
+        e[3] = cadd(a2, rot(b2, !INV));
+    }
+}
+
+template <int R0>
+__device__ void r0_forward(const FilterArgs& a, float2* x, const RowPair& rp) {
+    const int N2 = a.N2;
+    for (int j = threadIdx.x; j < N2; j += blockDim.x) {
+        float2 e[R0];
+#pragma unroll
+        for (int m = 0; m < R0; ++m) e[m] = rp.load(j + m * N2);
+        dft_small<R0, false>(e);
+        x[swz(j)] = e[0];
+#pragma unroll
+        for (int m = 1; m < R0; ++m) x[swz(m * N2 + j)] = cmul(e[m], __ldg(a.twr + (m - 1) * N2 + j));
+    }
+}
+
+template <int R0>
+__device__ void r0_inverse(const FilterArgs& a, const float2* x, const RowPair& rp) {
+    const int N2 = a.N2;
+    for (int j = threadIdx.x; j < N2; j += blockDim.x) {
+        float2 e[R0];
+        e[0] = x[swz(j)];
+#pragma unroll
+        for (int m = 1; m < R0; ++m) e[m] = cmulc(x[swz(m * N2 + j)], __ldg(a.twr + (m - 1) * N2 + j));
+        dft_small<R0, true>(e);
+#pragma unroll
+        for (int m = 0; m < R0; ++m) rp.store(j + m * N2, e[m]);
+    }
+}
+
 __global__ void __launch_bounds__(256) bp_ramp_filter_kernel(const __grid_constant__ FilterArgs a) {
     extern __shared__ __align__(16) float2 fx[];
     const int y = (int)blockIdx.y;
@@ -258,7 +326,29 @@ __global__ void __launch_bounds__(256) bp_ramp_filter_kernel(const __grid_consta
 
     const int ng = a.ngroups;
     int lm = 0;
-    while ((1 << lm) < a.M) ++lm;
+    while ((1 << lm) < a.N2) ++lm;
+    if (a.R0 > 1) {
+        // mixed radix: leading radix-R0 pass from HBM, radix-2 passes inside the R0
+        // blocks of N2, the fused middle, the inverse radix-2 passes, then radix-R0 to HBM
+        if (a.R0 == 3) r0_forward<3>(a, fx, rp); else r0_forward<5>(a, fx, rp);
+        __syncthreads();
+        int lg = lm;
+        for (int gi = 0; gi < ng - 1; ++gi) {
+            lg -= a.r[gi];
+            run_pass<0, false, false>(a.r[gi], a, fx, rp, lg, a.tw + a.twoff[gi]);
+            __syncthreads();
+        }
+        run_pass<1, false, false>(a.r[ng - 1], a, fx, rp, 0, nullptr);
+        lg = 0;
+        for (int gi = ng - 2; gi >= 0; --gi) {
+            __syncthreads();
+            lg += a.r[gi + 1];
+            run_pass<2, false, false>(a.r[gi], a, fx, rp, lg, a.tw + a.twoff[gi]);
+        }
+        __syncthreads();
+        if (a.R0 == 3) r0_inverse<3>(a, fx, rp); else r0_inverse<5>(a, fx, rp);
+        return;
+    }
     // forward passes; g_i = M >> (r_0 + ... + r_i); the last one (g = 1) is fused
     // with the H multiply and the first inverse pass
     if (ng == 1) {  // M <= 16: one pass from HBM to HBM
@@ -297,7 +387,7 @@ int launch_ramp_filter(const FilterArgs& a, int nviews, cudaStream_t stream) {
             bp_ramp_filter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return (int)e;
     }
-    const int threads = a.M / 16 >= 256 ? 256 : (a.M / 16 >= 32 ? a.M / 16 : 32);
+    const int threads = a.M / 16 >= 256 ? 256 : (a.M / 16 >= 32 ? (a.M / 16 + 31) / 32 * 32 : 32);
     dim3 grid((unsigned)((rows + 1) / 2), (unsigned)nviews);
     bp_ramp_filter_kernel<<<grid, threads, smem, stream>>>(a);
     return (int)cudaGetLastError();

@@ -29,18 +29,52 @@ int round_up(int v, int m) { return (v + m - 1) / m * m; }
 
 RampFilter::RampFilter(int isx, int isy, double sid, double sdd, double pitch) {
     if (isx > bpg::kMaxFilterM / 2) throw bph::config_error("filter: detector wider than 8192 pixels");
-    const bph::RampSpectrum rs = bph::ramp_spectrum(isx, sid, sdd, pitch);
-    const int M = rs.M;
+    if (isx < 2) throw bph::config_error("detector must be at least 2 pixels wide");
+    if (!(sid > 0) || !(sdd > 0) || !(pitch > 0)) throw bph::config_error("filter geometry must be positive");
+    // FFT length: the linear convolution of isx samples with the (2 isx - 1)-tap kernel
+    // needs M >= 2 isx - 1.  Mixed radix M = R0 * 2^q (R0 in {1, 3, 5}, 2^q >= 16 when
+    // R0 > 1) takes the smallest such length: 2560 instead of 4096 at isx = 1248.
+    const int need = 2 * isx - 1;
+    int M = 0, R0 = 1;
+    for (int r0 : {1, 3, 5})
+        for (int n2 = (r0 == 1 ? 2 : 16); (long long)r0 * n2 <= bpg::kMaxFilterM; n2 *= 2)
+            if (r0 * n2 >= need) {
+                if (M == 0 || r0 * n2 < M) { M = r0 * n2; R0 = r0; }
+                break;
+            }
+    if (const char* e = std::getenv("BP_FILTER_POW2"))  // A/B: force the radix-2 length
+        if (std::atoi(e)) {
+            M = 2;
+            while (M < need) M *= 2;
+            R0 = 1;
+        }
+    const int N2 = M / R0;
     int q = 0;
-    while ((1 << q) < M) ++q;
-    // register passes of <= 4 radix-2 stages; the leading pass takes the remainder
+    while ((1 << q) < N2) ++q;
+    // spectrum of the zero-padded Ram-Lak kernel (bph::ramp_spectrum's h), real since h
+    // is even: H[k] = sum_n h[n] cos(2 pi k n / M), in double
+    const double tau = pitch * sid / sdd;
+    std::vector<double> h((size_t)isx);
+    for (int n = 0; n < isx; ++n)
+        h[(size_t)n] = n == 0 ? 1.0 / (4.0 * tau * tau)
+                              : ((n & 1) ? -1.0 / (M_PI * M_PI * (double)n * (double)n * tau * tau) : 0.0);
+    std::vector<double> ctab((size_t)M), H((size_t)M);
+    for (int t = 0; t < M; ++t) ctab[(size_t)t] = std::cos(2.0 * M_PI * (double)t / (double)M);
+    for (int k = 0; k < M; ++k) {
+        double acc = h[0];
+        for (int n = 1; n < isx; n += 2) acc += 2.0 * h[(size_t)n] * ctab[(size_t)((long long)k * n % M)];
+        H[(size_t)k] = acc;
+    }
+    // register passes of <= 4 radix-2 stages over N2; the leading pass takes the remainder
     base_.ngroups = 0;
     int lead = q % 4 == 0 ? 4 : q % 4;
     if (q < 4) lead = q;
     base_.r[base_.ngroups++] = lead;
     for (int left = q - lead; left > 0; left -= 4) base_.r[base_.ngroups++] = 4;
-    // per-pass twiddle bases alpha_{i,j,s} = exp(-2 pi i j / (2 g_i 2^s)) = W_M^(j M / (2 g_i 2^s)),
-    // taken from the double-precision table (bp_filter.cu twiddle())
+    // per-pass twiddle bases alpha_{i,j,s} = exp(-2 pi i j / (2 g_i 2^s)) (bp_filter.cu twiddle())
+    auto w = [](double frac) {  // exp(-2 pi i frac)
+        return make_float2((float)std::cos(2.0 * M_PI * frac), (float)-std::sin(2.0 * M_PI * frac));
+    };
     std::vector<float2> tw;
     int lg = q;
     for (int i = 0; i < base_.ngroups; ++i) {
@@ -48,24 +82,34 @@ RampFilter::RampFilter(int isx, int isy, double sid, double sdd, double pitch) {
         base_.twoff[i] = (int)tw.size();
         const int g = 1 << lg;
         for (int j = 0; j < g; ++j)
-            for (int s = 0; s < base_.r[i]; ++s) {
-                const size_t k = (size_t)j * (size_t)M / ((size_t)2 * g << s);
-                tw.push_back(make_float2((float)rs.tw[k].real(), (float)rs.tw[k].imag()));
-            }
+            for (int s2 = 0; s2 < base_.r[i]; ++s2)
+                tw.push_back(w((double)j / (double)((long long)2 * g << s2)));
     }
+    // leading radix-R0 twiddles W_M^(j m'), m' in [1, R0)
+    std::vector<float2> twr;
+    for (int m = 1; m < R0; ++m)
+        for (int j = 0; j < N2; ++j) twr.push_back(w((double)((long long)j * m % M) / (double)M));
+    // H in the forward network's output order: sigma(m' N2 + j) = m' + R0 * bitrev_q(j)
     std::vector<float> hp((size_t)M);
-    for (int p = 0; p < M; ++p) {
-        int rev = 0;
-        for (int b = 0; b < q; ++b) rev |= ((p >> b) & 1) << (q - 1 - b);
-        hp[(size_t)p] = (float)(rs.H[(size_t)rev] * rs.tau / (double)M);
-    }
-    check(cudaMalloc(&d_tw_, tw.size() * sizeof(float2)), "cudaMalloc(filter)");
+    for (int mp = 0; mp < R0; ++mp)
+        for (int j = 0; j < N2; ++j) {
+            int rev = 0;
+            for (int b = 0; b < q; ++b) rev |= ((j >> b) & 1) << (q - 1 - b);
+            hp[(size_t)mp * N2 + j] = (float)(H[(size_t)(mp + R0 * rev)] * tau / (double)M);
+        }
+    check(cudaMalloc(&d_tw_, (tw.size() + twr.size() + 1) * sizeof(float2)), "cudaMalloc(filter)");
     check(cudaMalloc(&d_h_, hp.size() * sizeof(float)), "cudaMalloc(filter)");
     check(cudaMemcpy(d_tw_, tw.data(), tw.size() * sizeof(float2), cudaMemcpyHostToDevice), "filter");
+    if (!twr.empty())
+        check(cudaMemcpy(d_tw_ + tw.size(), twr.data(), twr.size() * sizeof(float2), cudaMemcpyHostToDevice),
+              "filter");
     check(cudaMemcpy(d_h_, hp.data(), hp.size() * sizeof(float), cudaMemcpyHostToDevice), "filter");
     base_.isx = isx;
     base_.M = M;
+    base_.R0 = R0;
+    base_.N2 = N2;
     base_.tw = d_tw_;
+    base_.twr = d_tw_ + tw.size();
     base_.hperm = d_h_;
     base_.sdd = sdd;
     base_.cu = 0.5 * (isx - 1);
