@@ -10,7 +10,9 @@
 //
 // One CTA filters one PAIR of detector rows: they are packed as the real and
 // imaginary parts of one complex row (H is real, so the two rows stay separate).
-// The M-point FFT runs in shared memory as a radix-2 network grouped into
+// M is the smallest R0 * 2^q >= 2 isx - 1 with R0 in {1, 3, 5} (2560 at isx = 1248); a
+// non-power-of-two M adds a leading radix-R0 pass (r0_forward / r0_inverse below).
+// The 2^q-point part runs in shared memory as a radix-2 network grouped into
 // register passes of up to 4 stages (16 elements per thread):
 //   * forward: decimation-in-frequency, natural order in -> bit-reversed out;
 //   * multiply by H, pre-permuted to bit-reversed order on the host;
