@@ -420,3 +420,37 @@ def test_multi_device_threads_on_one_gpu():
         assert rs.thread_updates_min + rs.thread_updates_max == rs.voxel_updates
     finally:
         bp.set_devices([0])
+
+
+def test_concurrent_bp_reconstruct_calls_from_threads():
+    # reentrant across contexts (SURVEY 8b threading row): two host threads call
+    # bp_reconstruct at once on different stacks; results equal the serial ones and a
+    # failing call's message stays on its own thread (thread-local bp_last_error)
+    import threading
+    pa, ma = baseline_small(n_views=12, shrink=8, seed=1)
+    pb, mb = baseline_small(n_views=12, shrink=8, seed=2)
+    sa, sb = bp.Stack.from_arrays(pa, ma), bp.Stack.from_arrays(pb, mb)
+    ref_a, _ = bp.reconstruct(sa, bp.recon_params(32))
+    ref_b, _ = bp.reconstruct(sb, bp.recon_params(32))
+    ra, rb = ref_a.data.copy(), ref_b.data.copy()
+    out, errs = {}, {}
+
+    def work(name, st, p):
+        try:
+            for _ in range(3):
+                v, _ = bp.reconstruct(st, p)
+                out[name] = v.data.copy()
+        except bp.BPError as e:
+            errs[name] = (e.code, str(e))
+
+    bad = bp.recon_params(32, lanes=5)  # BP_EINVAL in this thread only
+    ts = [threading.Thread(target=work, args=("a", sa, bp.recon_params(32))),
+          threading.Thread(target=work, args=("b", sb, bp.recon_params(32))),
+          threading.Thread(target=work, args=("c", sa, bad))]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    assert bitwise_equal(out["a"], ra) and bitwise_equal(out["b"], rb)
+    assert errs.get("c", (None,))[0] == bp.BP_EINVAL and "lane" in errs["c"][1]
+    assert "a" not in errs and "b" not in errs
