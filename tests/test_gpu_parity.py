@@ -454,3 +454,15 @@ def test_concurrent_bp_reconstruct_calls_from_threads():
     assert bitwise_equal(out["a"], ra) and bitwise_equal(out["b"], rb)
     assert errs.get("c", (None,))[0] == bp.BP_EINVAL and "lane" in errs["c"][1]
     assert "a" not in errs and "b" not in errs
+
+
+@pytest.mark.parametrize("isx,isy,L", [(58, 47, 32), (250, 173, 64), (2048, 64, 128)])
+def test_strict_bitwise_odd_and_wide_detectors(isx, isy, L):
+    # pitch != isx (2-D H2D copies into a 16-B aligned ring), odd row counts, and a wide
+    # detector whose footprints exceed the tile (fallback pairs) -- all bitwise
+    s = bp.Stack.generate("spheres3", 5, isx, isy, 750.0, 1200.0, 0.32 * 1248.0 / isx)
+    px, mats = s.pixels.copy(), s.matrices.copy()
+    ref, _ = O.reconstruct(px, mats, L)
+    for kw in (dict(), dict(row_windows=False), dict(view_batch=2)):
+        got, st = gpu_recon(px, mats, L, **kw)
+        assert bitwise_equal(got, ref), (kw, err_stats(got, ref))
