@@ -78,3 +78,22 @@ def test_config2_256_full_volume_strict_bitwise(stack):
     assert st.fallback_pairs == 0 and st.tile_pairs > 0
     ref, _ = O.reconstruct(stack.pixels, stack.matrices, L)
     assert bitwise_equal(got, ref)
+
+
+def test_partial_blocks_at_large_odd_multiple_edge():
+    # L = 520 is not a multiple of the 32x32x8 block in x/y, and L = 514 is not one in z
+    # either: the masked edge blocks stay bitwise on sampled lines, fast mode in tolerance
+    from tests.helpers import baseline_small
+    px, mats = baseline_small(n_views=24, shrink=1)
+    st = bp.Stack.from_arrays(px, mats)
+    for L in (520, 514):
+        ys, zs = _lines(L, 16, L)
+        ys[4:8] = L - 1 - np.arange(4)   # last, partially covered block rows
+        zs[4:8] = L - 1 - np.arange(4)
+        with bp.GpuContext(L, 1248, 960, device=0, strict=True) as c:
+            c.backproject_stack(st)
+            _, s1 = c.finish(readback=False)
+            got = c.read_lines(ys, zs)
+        ref = O.reconstruct_lines(px, mats, L, ys, zs)
+        assert s1.fallback_pairs == 0
+        assert bitwise_equal(got, ref), L
