@@ -82,7 +82,7 @@ def test_config2_256_full_volume_strict_bitwise(stack):
 
 def test_partial_blocks_at_large_odd_multiple_edge():
     # L = 520 is not a multiple of the 32x32x8 block in x/y, and L = 514 is not one in z
-    # either: the masked edge blocks stay bitwise on sampled lines, fast mode in tolerance
+    # either: the masked edge blocks stay bitwise on sampled lines
     from tests.helpers import baseline_small
     px, mats = baseline_small(n_views=24, shrink=1)
     st = bp.Stack.from_arrays(px, mats)
