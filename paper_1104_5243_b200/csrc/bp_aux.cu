@@ -1,0 +1,195 @@
+// bp_aux.cu -- auxiliary kernels around the backprojection: the exact visible-update
+// count and per-line clip ranges (precompute.cpp:19-103), the reciprocal self-test, and
+// the on-device volume comparison used by the full-size parity tests.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstring>
+
+#include "bp_device.hpp"
+#include "bp_device_math.cuh"
+
+namespace bpg {
+
+// ---------------------------------------------------------------------------
+// Exact visible-update count (LineProjector::visible, precompute.cpp:37-46):
+// one thread per (view, z, y) line, scanning x from both ends like
+// build_clip_table (precompute.cpp:68-80).
+
+__global__ void bp_clip_count_kernel(const __grid_constant__ SlabArgs s,
+                                     const __grid_constant__ BatchArgs b) {
+    const long long lines = (long long)s.nz * s.L;
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    const int k = blockIdx.y;
+    unsigned long long vis = 0;
+    if (i < lines) {
+        const int y = (int)(i % s.L);
+        const int z = s.z0 + (int)(i / s.L);
+        const float* A = b.A[k];
+        float uy, vy, wy_;
+        line_consts(A, s.wy[y], s.wz[z], uy, vy, wy_);
+        const float hu = (float)s.isx, hv = (float)s.isy;
+        auto visible = [&](int x) {
+            const float wx = s.wx[x];
+            const float w = __fadd_rn(__fmul_rn(A[2], wx), wy_);
+            const float r = __frcp_rn(w);
+            float u = __fmul_rn(__fadd_rn(__fmul_rn(A[0], wx), uy), r);
+            u = (u < -2.0f) ? -2.0f : u;
+            u = (hu < u) ? hu : u;
+            float v = __fmul_rn(__fadd_rn(__fmul_rn(A[1], wx), vy), r);
+            v = (v < -2.0f) ? -2.0f : v;
+            v = (hv < v) ? hv : v;
+            const int iu = (int)floorf(u), iv = (int)floorf(v);
+            return iu >= -1 && iu <= s.isx - 1 && iv >= -1 && iv <= s.isy - 1;
+        };
+        int f = 0;
+        while (f < s.L && !visible(f)) ++f;
+        if (f < s.L) {
+            int l = s.L - 1;
+            while (l > f && !visible(l)) --l;
+            vis = (unsigned long long)(l - f + 1);
+        }
+    }
+    // warp reduce then one atomic per warp
+    for (int o = 16; o; o >>= 1) vis += __shfl_xor_sync(0xffffffffu, vis, o);
+    if ((threadIdx.x & 31) == 0 && vis) atomicAdd(s.counters + 3, vis);
+}
+
+// Per-line clip ranges in the reference's BPCT layout (precompute.cpp:51-91,
+// precompute.hpp:14-25): ranges[2*((p*L + z)*L + y)] = first, last; empty lines
+// are (0xFFFF, 0).  Same exact float replay as bp_clip_count_kernel.
+__global__ void bp_clip_ranges_kernel(const __grid_constant__ SlabArgs s,
+                                      const __grid_constant__ BatchArgs b, uint16_t* ranges,
+                                      int view0) {
+    const long long lines = (long long)s.nz * s.L;
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    const int k = blockIdx.y;
+    if (i >= lines) return;
+    const int y = (int)(i % s.L);
+    const int z = s.z0 + (int)(i / s.L);
+    const float* A = b.A[k];
+    float uy, vy, wy_;
+    line_consts(A, s.wy[y], s.wz[z], uy, vy, wy_);
+    const float hu = (float)s.isx, hv = (float)s.isy;
+    auto visible = [&](int x) {
+        const float wx = s.wx[x];
+        const float w = __fadd_rn(__fmul_rn(A[2], wx), wy_);
+        const float r = __frcp_rn(w);
+        float u = __fmul_rn(__fadd_rn(__fmul_rn(A[0], wx), uy), r);
+        u = (u < -2.0f) ? -2.0f : u;
+        u = (hu < u) ? hu : u;
+        float v = __fmul_rn(__fadd_rn(__fmul_rn(A[1], wx), vy), r);
+        v = (v < -2.0f) ? -2.0f : v;
+        v = (hv < v) ? hv : v;
+        const int iu = (int)floorf(u), iv = (int)floorf(v);
+        return iu >= -1 && iu <= s.isx - 1 && iv >= -1 && iv <= s.isy - 1;
+    };
+    int f = 0;
+    while (f < s.L && !visible(f)) ++f;
+    uint16_t first = 0xFFFF, last = 0;
+    if (f < s.L) {
+        int l = s.L - 1;
+        while (l > f && !visible(l)) --l;
+        first = (uint16_t)f;
+        last = (uint16_t)l;
+    }
+    const size_t idx = 2 * (((size_t)(view0 + k) * s.L + z) * s.L + y);
+    ranges[idx] = first;
+    ranges[idx + 1] = last;
+}
+
+int launch_clip_ranges(const SlabArgs& s, const BatchArgs& b, uint16_t* ranges, int view0,
+                       void* stream) {
+    const long long lines = (long long)s.nz * s.L;
+    dim3 grid((unsigned)((lines + 255) / 256), (unsigned)b.nviews);
+    bp_clip_ranges_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(s, b, ranges, view0);
+    return (int)cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// Self-test: the paired MUFU+Newton reciprocal against __frcp_rn (== IEEE
+// 1.0f/w) over every float bit pattern in [lo_bits, hi_bits).
+
+__global__ void bp_rcp_selftest_kernel(uint32_t lo, uint32_t hi, unsigned long long* bad) {
+    unsigned long long nbad = 0;
+    for (uint32_t i = lo + 2u * (blockIdx.x * blockDim.x + threadIdx.x); i < hi;
+         i += 2u * gridDim.x * blockDim.x) {
+        const float a = __uint_as_float(i);
+        const float b = __uint_as_float(i + 1 < hi ? i + 1 : i);
+        const f2 r = rcp2_rn(f2{a, b});
+        nbad += (__float_as_uint(r.x) != __float_as_uint(__frcp_rn(a)));
+        nbad += (__float_as_uint(r.y) != __float_as_uint(__frcp_rn(b)));
+    }
+    for (int o = 16; o; o >>= 1) nbad += __shfl_xor_sync(0xffffffffu, nbad, o);
+    if ((threadIdx.x & 31) == 0 && nbad) atomicAdd(bad, nbad);
+}
+
+int selftest_rcp(uint32_t lo_bits, uint32_t hi_bits, unsigned long long* mismatches) {
+    unsigned long long* d = nullptr;
+    cudaError_t e = cudaMalloc(&d, sizeof *d);
+    if (e != cudaSuccess) return (int)e;
+    cudaMemset(d, 0, sizeof *d);
+    bp_rcp_selftest_kernel<<<148 * 8, 256>>>(lo_bits, hi_bits, d);
+    e = cudaGetLastError();
+    if (e == cudaSuccess) e = cudaMemcpy(mismatches, d, sizeof *d, cudaMemcpyDeviceToHost);
+    cudaFree(d);
+    return (int)e;
+}
+
+// ---------------------------------------------------------------------------
+// Diagnostic comparison (full-size property tests without host transfers).
+
+__global__ void bp_compare_kernel(const float* a, const float* b, unsigned long long n,
+                                  double* out, unsigned long long* nbit) {
+    double mx = 0.0, mr = 0.0, ss = 0.0;
+    unsigned long long nb = 0;
+    for (unsigned long long i = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; i < n;
+         i += (unsigned long long)gridDim.x * blockDim.x) {
+        const float x = a[i], y = b[i];
+        const double d = (double)x - (double)y;
+        mx = fmax(mx, fabs(d));
+        mr = fmax(mr, fabs((double)y));
+        ss += d * d;
+        nb += (__float_as_uint(x) != __float_as_uint(y));
+    }
+    for (int o = 16; o; o >>= 1) {
+        mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        mr = fmax(mr, __shfl_xor_sync(0xffffffffu, mr, o));
+        ss += __shfl_xor_sync(0xffffffffu, ss, o);
+        nb += __shfl_xor_sync(0xffffffffu, nb, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        // max of non-negative doubles via their ordered bit patterns
+        atomicMax(reinterpret_cast<unsigned long long*>(out + 0), (unsigned long long)__double_as_longlong(mx));
+        atomicMax(reinterpret_cast<unsigned long long*>(out + 1), (unsigned long long)__double_as_longlong(mr));
+        atomicAdd(out + 2, ss);
+        atomicAdd(nbit, nb);
+    }
+}
+
+int device_compare(const float* a, const float* b, unsigned long long n, double* res3,
+                   unsigned long long* nbit) {
+    double* d = nullptr;
+    cudaError_t e = cudaMalloc(&d, 4 * sizeof(double));
+    if (e != cudaSuccess) return (int)e;
+    cudaMemset(d, 0, 4 * sizeof(double));
+    bp_compare_kernel<<<148 * 8, 256>>>(a, b, n, d, reinterpret_cast<unsigned long long*>(d + 3));
+    e = cudaGetLastError();
+    double h[4] = {0, 0, 0, 0};
+    if (e == cudaSuccess) e = cudaMemcpy(h, d, sizeof h, cudaMemcpyDeviceToHost);
+    cudaFree(d);
+    res3[0] = h[0];
+    res3[1] = h[1];
+    res3[2] = h[2];
+    std::memcpy(nbit, &h[3], sizeof *nbit);
+    return (int)e;
+}
+
+int launch_clip_count(const SlabArgs& s, const BatchArgs& b, void* stream) {
+    const long long lines = (long long)s.nz * s.L;
+    dim3 grid((unsigned)((lines + 255) / 256), (unsigned)b.nviews);
+    bp_clip_count_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(s, b);
+    return (int)cudaGetLastError();
+}
+
+}  // namespace bpg
