@@ -462,12 +462,11 @@ def run_ours(args):
                                  "views) / live mean launch time; ncu agrees (profiles/latest.json). HBM is "
                                  "not the bound"},
                      "binding_unit": {
-                         "unit": "LSU shared-memory wavefronts (1 per clk per SM)",
+                         "unit": "co-limit: LSU shared-memory wavefronts (1 per clk per SM) and FMA-pipe issue",
                          "util": prof.get("lsu_wavefronts_pct", 0.0) / 100.0,
                          "fma_pipe_util": prof.get("fma_pipe_active_pct", 0.0) / 100.0,
-                         "source": "ncu --set full of the same kernel (profiles/latest.json): 0.236 "
-                                   "wavefronts per computed update, of which 0.071 are bank-conflict "
-                                   "replays (DESIGN.md 3.5)"}},
+                         "source": "ncu --set full of the same kernel (profiles/latest.json); at the margin "
+                                   "time follows FMA-pipe work, not conflict replays (DESIGN.md 3.5)"}},
         "e2e": {"value": e2e_val, "unit": "GUP/s", "h2d_bytes_per_step": h2d // args.steps,
                 "d2h_bytes_per_step": d2h // args.steps,
                 "ms_per_step": e2e_s * 1e3 / args.steps,
