@@ -192,4 +192,38 @@ int launch_clip_count(const SlabArgs& s, const BatchArgs& b, void* stream) {
     return (int)cudaGetLastError();
 }
 
+// ---------------------------------------------------------------------------
+// Pair ring for the fast-mode kernel ("pair ring"): pair row e of a
+// slot holds, per column c, (p[e-1][c], p[e][c] - p[e-1][c]) with p[-1] = p[isy] = 0,
+// the zero border of pad_image (kernel.cpp:32-47).  The fast kernel's vertical lerp
+// fma(sy, bl - tl, tl) then needs one 8-byte load per column and no subtraction;
+// bl - tl is the same IEEE subtraction the kernel would do, so results are bitwise
+// those of the raw-tile fast kernel.  One block per (pair row, view), float4 in,
+// 2 x float4 out: HBM-bound (4 + 8 bytes per texel).
+__global__ void __launch_bounds__(320) bp_expand_kernel(const __grid_constant__ ExpandArgs a) {
+    const int e = blockIdx.x;
+    const size_t slot = (size_t)a.slot[blockIdx.y];
+    const float* img = a.ring + slot * a.isy * a.pitch;
+    const float4* up = reinterpret_cast<const float4*>(img + (size_t)(e - 1) * a.pitch);
+    const float4* dn = reinterpret_cast<const float4*>(img + (size_t)e * a.pitch);
+    float4* out = reinterpret_cast<float4*>(a.ringx + (slot * (a.isy + 1) + e) * a.pitchx);
+    const bool has_up = e > 0, has_dn = e < a.isy;
+    const int n4 = a.pitch / 4;
+    for (int c = threadIdx.x; c < n4; c += blockDim.x) {
+        const float4 zero = make_float4(0.f, 0.f, 0.f, 0.f);
+        const float4 p = has_up ? __ldg(up + c) : zero;
+        const float4 q = has_dn ? __ldg(dn + c) : zero;
+        out[2 * c] = make_float4(p.x, __fsub_rn(q.x, p.x), p.y, __fsub_rn(q.y, p.y));
+        out[2 * c + 1] = make_float4(p.z, __fsub_rn(q.z, p.z), p.w, __fsub_rn(q.w, p.w));
+    }
+}
+
+int launch_expand(const ExpandArgs& a, int n, void* stream) {
+    if (n < 1) return 0;
+    if (a.pitch % 4 || a.pitchx < a.pitch) return (int)cudaErrorInvalidValue;
+    dim3 grid((unsigned)(a.isy + 1), (unsigned)n);
+    bp_expand_kernel<<<grid, 320, 0, (cudaStream_t)stream>>>(a);
+    return (int)cudaGetLastError();
+}
+
 }  // namespace bpg

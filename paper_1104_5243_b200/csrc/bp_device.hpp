@@ -51,10 +51,12 @@ enum KernelKind : int { kKernelAuto = 0, kKernelSimple = 1 };
 
 struct TileShape {
     int bx, by, bz;              // voxel block
-    int tw, th;                  // tile pitch (floats, % 4 == 0) and ring rows (% 8 == 0)
+    int tw, th;                  // tile pitch (texels; % 4 == 0, % 2 for dy) and ring rows (% 8 == 0)
     int stages;
     int threads;                 // consumer + producer threads per CTA
     int smem_bytes;
+    int dy;                      // 1: fast-mode kernel over the pair ring (p, p_down - p),
+                                 //    8-byte texels ("pair ring")
 };
 
 // Picks the tiled-kernel variant for edge length L (returns false if the
@@ -65,6 +67,23 @@ bool tile_shape_for(int L, TileShape* out);
 // Returns 0 on success.
 int encode_ring_tmap(void* tmap128, const float* ring, int isx, int isy, int pitch, int slots,
                      const TileShape& ts, char* err, int errlen);
+
+// Same over the pair ring [slots][isy + 1][pitchx] float2 (8-byte texels): pair row e
+// holds (p[e-1][c], p[e][c] - p[e-1][c]) with zero rows at e-1 = -1 and e = isy.
+int encode_pair_tmap(void* tmap128, const float2* ringx, int isx, int isy, int pitchx, int slots,
+                     const TileShape& ts, char* err, int errlen);
+
+// Builds pair rows [0, isy] of n ring slots from the raw float ring (bp_aux.cu).
+struct ExpandArgs {
+    const float* ring;
+    float2* ringx;
+    int isx, isy, pitch, pitchx;  // pitch, pitchx: multiples of 4 (floats / float2)
+    int slot[kMaxBatch];
+};
+int launch_expand(const ExpandArgs& a, int n, void* stream);
+
+// True when a pair-ring (dy) variant exists for this block shape.
+bool has_pair_variant(const TileShape& ts);
 
 int launch_tiled(const void* tmap128, const SlabArgs& s, const BatchArgs& b,
                  const TileShape& ts, bool strict, bool distance_weight, bool hw_rcp, void* stream);

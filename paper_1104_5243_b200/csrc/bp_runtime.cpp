@@ -165,6 +165,28 @@ void SlabContext::filter_pending(Pending& p) {
     p.filtered = true;
 }
 
+void SlabContext::expand(const bpg::BatchArgs& b) {
+    if (!tiled_ || !ts_.dy) return;
+    bpg::ExpandArgs a{};
+    a.ring = d_ring_;
+    a.ringx = d_ringx_;
+    a.isx = isx_;
+    a.isy = isy_;
+    a.pitch = pitch_;
+    a.pitchx = pitch_;
+    for (int i = 0; i < b.nviews; ++i) a.slot[i] = b.slot[i];
+    check((cudaError_t)bpg::launch_expand(a, b.nviews, s_comp_), "pair ring expansion");
+    expanded_views_ += (uint64_t)b.nviews;
+}
+
+void SlabContext::expand_pending(Pending& p) {
+    // after filter_pending (the pair ring is built from the filtered rows), once per
+    // batch even when the deferred tail launches it once per z-chunk
+    if (p.expanded) return;
+    expand(p.b);
+    p.expanded = true;
+}
+
 void SlabContext::mark_t0() {
     if (!t0_rec_) {
         check(cudaEventRecord(ev_t0_, s_comp_), "event");
@@ -210,6 +232,7 @@ SlabContext::SlabContext(const bp_gpu_config& cfg) : cfg_(cfg) {
     if (const char* e = std::getenv("BP_TAIL_BATCHES")) tail_batches_ = std::max(0, std::atoi(e));
     if (const char* e = std::getenv("BP_TAIL_CHUNKS")) tail_chunks_ = std::max(1, std::atoi(e));
     if (const char* e = std::getenv("BP_H2D_RUN_MB")) run_limit_ = (size_t)std::max(0, std::atoi(e)) << 20;
+    if (const char* e = std::getenv("BP_NO_PAIR")) pair_ok_ = std::atoi(e) == 0;
     out_vol_ = cfg.output_volume;
     // the final batch must be launched by finish(), which knows it is the last
     if (out_vol_) tail_batches_ = std::max(tail_batches_, 1);
@@ -251,6 +274,7 @@ SlabContext::SlabContext(const bp_gpu_config& cfg) : cfg_(cfg) {
     for (cudaEvent_t* e : {&ev_t0_, &ev_t1_, &ev_h0_, &ev_h1_, &ev_d0_, &ev_d1_})
         check(cudaEventCreate(e), "event");
     std::memset(tmap_, 0, sizeof tmap_);
+    std::memset(tmapx_, 0, sizeof tmapx_);
     if (cfg.filter) filt_ = std::make_unique<RampFilter>(isx_, isy_, cfg.sid_mm, cfg.sdd_mm, cfg.pitch_mm);
     reset_recon();
 }
@@ -274,6 +298,7 @@ SlabContext::~SlabContext() {
     if (s_d2h_) cudaStreamDestroy(s_d2h_);
     if (own_vol_ && d_vol_) cudaFree(d_vol_);
     cudaFree(d_ring_);
+    if (d_ringx_) cudaFree(d_ringx_);
     cudaFree(d_wx_);
     cudaFree(d_wy_);
     cudaFree(d_wz_);
@@ -389,6 +414,8 @@ void SlabContext::choose_tile(const bpg::BatchArgs& b) {
         tiled_ = false;
         return;
     }
+    // fast mode reads the pair ring where a pair variant exists
+    t.dy = (!cfg_.strict_mode && pair_ok_ && bpg::has_pair_variant(t)) ? 1 : 0;
     // Sample the block lattice (including the outermost blocks, whose shadows
     // are the largest) for a few views of this batch; size the SMEM tile from
     // the largest footprint plus a guard.  Pairs that still do not fit are
@@ -443,7 +470,9 @@ void SlabContext::choose_tile(const bpg::BatchArgs& b) {
     // compile-time pitches (== 16 mod 32: immediate row offsets, low conflicts); the
     // smallest listed one that holds the footprint
     int twcs[3] = {0, 0, 0};
-    if (t.bx == 64) {
+    if (t.dy) {
+        twcs[0] = 152;  // 8-byte texels, == 8 (mod 16): lowest simulated conflicts
+    } else if (t.bx == 64) {
         twcs[0] = 240;
     } else if (t.by == 32) {
         twcs[0] = 176;  // narrower 112 at 1024^3 measured 0.9% slower (A/B)
@@ -456,6 +485,9 @@ void SlabContext::choose_tile(const bpg::BatchArgs& b) {
     if (const char* e = std::getenv("BP_TWC")) twc = std::atoi(e);
     if (twc_ok && twc > 0 && tw <= twc) {
         tw = twc;
+    } else if (t.dy) {
+        tw = round_up(tw, 8);
+        if (tw % 16 != 8) tw += 8;
     } else if (tw % 32 != 20) {
         const int t2 = tw + ((20 - tw % 32) + 32) % 32;
         if (t2 <= 256) tw = t2;
@@ -481,6 +513,14 @@ void SlabContext::choose_tile(const bpg::BatchArgs& b) {
     char err[256];
     if (bpg::encode_ring_tmap(tmap_, d_ring_, isx_, isy_, pitch_, slots_, t, err, sizeof err) != 0)
         throw bph::device_error(err);
+    if (t.dy) {
+        if (!d_ringx_) {
+            const size_t n = (size_t)slots_ * (isy_ + 1) * pitch_;
+            check(cudaMalloc(&d_ringx_, n * sizeof(float2)), "cudaMalloc(pair ring)");
+        }
+        if (bpg::encode_pair_tmap(tmapx_, d_ringx_, isx_, isy_, pitch_, slots_, t, err, sizeof err) != 0)
+            throw bph::device_error(err);
+    }
     ts_ = t;
     tiled_ = true;
 }
@@ -525,7 +565,7 @@ void SlabContext::launch(const bpg::BatchArgs& b, int zc0, int zc1, bool final_p
     }
     int rc;
     if (tiled_)
-        rc = bpg::launch_tiled(tmap_, s, b, ts_, cfg_.strict_mode != 0, cfg_.distance_weight != 0,
+        rc = bpg::launch_tiled(ts_.dy ? tmapx_ : tmap_, s, b, ts_, cfg_.strict_mode != 0, cfg_.distance_weight != 0,
                                cfg_.recip_mode == BP_RECIP_HW_APPROX, s_comp_);
     else
         rc = bpg::launch_simple(s, b, cfg_.distance_weight != 0, cfg_.recip_mode, s_comp_);
@@ -540,6 +580,7 @@ void SlabContext::launch_pending_front(bool final_pass) {
     check(cudaStreamWaitEvent(s_comp_, ev_ready_[(size_t)p.rg], 0), "wait");
     mark_t0();
     filter_pending(p);
+    expand_pending(p);
     p.b.load_volume = p.index > 0 ? 1 : 0;
     launch(p.b, 0, -1, final_pass);
     any_launch_ = true;
@@ -582,7 +623,10 @@ void SlabContext::finish(float* host_volume, bp_gpu_stats* st) {
         for (const auto& p : pending_)
             check(cudaStreamWaitEvent(s_comp_, ev_ready_[(size_t)p.rg], 0), "wait");
         mark_t0();
-        for (auto& p : pending_) filter_pending(p);
+        for (auto& p : pending_) {
+            filter_pending(p);
+            expand_pending(p);
+        }
         for (int c = 0; c < C; ++c) {
             for (size_t i = 0; i < pending_.size(); ++i) {
                 auto p = pending_[i];
@@ -766,6 +810,7 @@ double SlabContext::time_resident(int iters, bp_gpu_stats* st) {
                 b.slot[i] = k0 + i;
             }
             choose_tile(b);
+            expand(b);  // inside the timed region: part of every reconstruction
             launch(b, 0, -1, k0 + B_ >= resident_);
         }
     }

@@ -83,8 +83,11 @@ private:
         uint64_t index;  // batch index within the reconstruction
         std::array<int, bpg::kMaxBatch> fr0, fr1;  // rows to filter per view (cfg_.filter)
         bool filtered = false;
+        bool expanded = false;
     };
     void filter_pending(Pending& p);
+    void expand_pending(Pending& p);
+    void expand(const bpg::BatchArgs& b);  // pair rows of the batch's slots (ts_.dy)
     void flush();
     void choose_tile(const bpg::BatchArgs& b);
     // launch over slab-local z range [zc0, zc1) (default: the whole slab)
@@ -125,6 +128,12 @@ private:
     bool tiled_ = false;
     bpg::TileShape ts_{};
     alignas(64) unsigned char tmap_[128];
+    // fast-mode pair ring: [slots][isy + 1][pitch] float2, built per
+    // batch from d_ring_ by bp_expand_kernel
+    bool pair_ok_ = true;  // BP_NO_PAIR=1 keeps the raw-tile fast kernel (A/B)
+    float2* d_ringx_ = nullptr;
+    alignas(64) unsigned char tmapx_[128];
+    uint64_t expanded_views_ = 0;
 
     // deferred tail: the last tail_batches_ batches are held back and, when the
     // volume is read back, processed z-chunk-major so each finished chunk's D2H
