@@ -199,8 +199,10 @@ int launch_clip_count(const SlabArgs& s, const BatchArgs& b, void* stream) {
 // fma(sy, bl - tl, tl) then needs one 8-byte load per column and no subtraction;
 // bl - tl is the same IEEE subtraction the kernel would do, so results are bitwise
 // those of the raw-tile fast kernel.  One block per (pair row, view), float4 in,
-// 2 x float4 out: HBM-bound (4 + 8 bytes per texel).
-__global__ void __launch_bounds__(320) bp_expand_kernel(const __grid_constant__ ExpandArgs a) {
+// 2 x float4 out: HBM-bound (4 + 8 bytes per texel).  128-thread blocks with few
+// registers fit beside two resident backprojection CTAs, so the expansion of the
+// next batch runs on a low-priority stream under the current batch's kernel.
+__global__ void __launch_bounds__(128) bp_expand_kernel(const __grid_constant__ ExpandArgs a) {
     const int e = blockIdx.x;
     const size_t slot = (size_t)a.slot[blockIdx.y];
     const float* img = a.ring + slot * a.isy * a.pitch;
@@ -222,7 +224,14 @@ int launch_expand(const ExpandArgs& a, int n, void* stream) {
     if (n < 1) return 0;
     if (a.pitch % 4 || a.pitchx < a.pitch) return (int)cudaErrorInvalidValue;
     dim3 grid((unsigned)(a.isy + 1), (unsigned)n);
-    bp_expand_kernel<<<grid, 320, 0, (cudaStream_t)stream>>>(a);
+    static const bool carve = [] {
+        // same shared-memory carveout as the backprojection kernel, so expansion
+        // blocks can be co-resident with it on an SM
+        return cudaFuncSetAttribute(bp_expand_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                    100) == cudaSuccess;
+    }();
+    (void)carve;
+    bp_expand_kernel<<<grid, 128, 0, (cudaStream_t)stream>>>(a);
     return (int)cudaGetLastError();
 }
 

@@ -153,19 +153,37 @@ void RampFilter::apply(float* d_img, long long view_stride, int pitch, int nview
     check((cudaError_t)bpg::launch_ramp_filter(a, nviews, s), "ramp filter launch");
 }
 
-void SlabContext::filter_pending(Pending& p) {
-    // FDK preprocessing of a batch's ring slots in place, one launch on the
-    // compute stream right before the batch's first backprojection launch (its
-    // uploads are complete by then), so it neither delays the copy stream nor
-    // stalls earlier, ready backprojection launches behind a pending upload
-    if (!filt_ || p.filtered) return;
-    filt_->apply_batch(d_ring_, (long long)isy_ * pitch_, pitch_, p.b.nviews, p.b.slot, p.fr0.data(),
-                       p.fr1.data(), s_comp_);
-    filtered_views_ += (uint64_t)p.b.nviews;
-    p.filtered = true;
+void SlabContext::prepare(Pending& p) {
+    // FDK preprocessing of the batch's ring slots in place, then the pair ring, on
+    // the low-priority prep stream once the batch's uploads are complete.  Neither
+    // delays the copy stream nor stalls earlier, ready backprojection launches; the
+    // backprojection of this batch waits on p.ready.  Done once per batch, even when
+    // the deferred tail launches it once per z-chunk.
+    if (p.ready) return;
+    const bool filt = filt_ && !p.filtered;
+    const bool expd = tiled_ && ts_.dy && !p.expanded;
+    if (!filt && !expd) {
+        p.ready = ev_ready_[(size_t)p.rg];
+        return;
+    }
+    mark_t0();  // the prep work belongs to the reconstruction's device time
+    check(cudaStreamWaitEvent(s_prep_, ev_t0_, 0), "wait");
+    check(cudaStreamWaitEvent(s_prep_, ev_ready_[(size_t)p.rg], 0), "wait");
+    if (filt) {
+        filt_->apply_batch(d_ring_, (long long)isy_ * pitch_, pitch_, p.b.nviews, p.b.slot,
+                           p.fr0.data(), p.fr1.data(), s_prep_);
+        filtered_views_ += (uint64_t)p.b.nviews;
+        p.filtered = true;
+    }
+    if (expd) {
+        expand(p.b, s_prep_);
+        p.expanded = true;
+    }
+    check(cudaEventRecord(ev_prep_[(size_t)p.rg], s_prep_), "event");
+    p.ready = ev_prep_[(size_t)p.rg];
 }
 
-void SlabContext::expand(const bpg::BatchArgs& b) {
+void SlabContext::expand(const bpg::BatchArgs& b, cudaStream_t st) {
     if (!tiled_ || !ts_.dy) return;
     bpg::ExpandArgs a{};
     a.ring = d_ring_;
@@ -175,16 +193,8 @@ void SlabContext::expand(const bpg::BatchArgs& b) {
     a.pitch = pitch_;
     a.pitchx = pitch_;
     for (int i = 0; i < b.nviews; ++i) a.slot[i] = b.slot[i];
-    check((cudaError_t)bpg::launch_expand(a, b.nviews, s_comp_), "pair ring expansion");
+    check((cudaError_t)bpg::launch_expand(a, b.nviews, st), "pair ring expansion");
     expanded_views_ += (uint64_t)b.nviews;
-}
-
-void SlabContext::expand_pending(Pending& p) {
-    // after filter_pending (the pair ring is built from the filtered rows), once per
-    // batch even when the deferred tail launches it once per z-chunk
-    if (p.expanded) return;
-    expand(p.b);
-    p.expanded = true;
 }
 
 void SlabContext::mark_t0() {
@@ -259,17 +269,22 @@ SlabContext::SlabContext(const bp_gpu_config& cfg) : cfg_(cfg) {
     check(cudaMemcpy(d_wz_, hwz.data(), tab * sizeof(float), cudaMemcpyHostToDevice), "tables");
     check(cudaMalloc(&d_cnt_, 8 * sizeof(unsigned long long)), "cudaMalloc(counters)");
     check(cudaMemset(d_cnt_, 0, 8 * sizeof(unsigned long long)), "cudaMemset(counters)");
-    check(cudaStreamCreateWithFlags(&s_comp_, cudaStreamNonBlocking), "stream");
+    int prio_lo = 0, prio_hi = 0;
+    check(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi), "stream priorities");
+    check(cudaStreamCreateWithPriority(&s_comp_, cudaStreamNonBlocking, prio_hi), "stream");
+    check(cudaStreamCreateWithPriority(&s_prep_, cudaStreamNonBlocking, prio_lo), "stream");
     check(cudaStreamCreateWithFlags(&s_copy_, cudaStreamNonBlocking), "stream");
     check(cudaStreamCreateWithFlags(&s_d2h_, cudaStreamNonBlocking), "stream");
     ev_chunk_.resize((size_t)tail_chunks_);
     for (auto& e : ev_chunk_) check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
     ev_ready_.resize((size_t)R_);
     ev_free_.resize((size_t)R_);
+    ev_prep_.resize((size_t)R_);
     used_.assign((size_t)R_, false);
     for (int i = 0; i < R_; ++i) {
         check(cudaEventCreateWithFlags(&ev_ready_[(size_t)i], cudaEventDisableTiming), "event");
         check(cudaEventCreateWithFlags(&ev_free_[(size_t)i], cudaEventDisableTiming), "event");
+        check(cudaEventCreateWithFlags(&ev_prep_[(size_t)i], cudaEventDisableTiming), "event");
     }
     for (cudaEvent_t* e : {&ev_t0_, &ev_t1_, &ev_h0_, &ev_h1_, &ev_d0_, &ev_d1_})
         check(cudaEventCreate(e), "event");
@@ -282,11 +297,13 @@ SlabContext::SlabContext(const bp_gpu_config& cfg) : cfg_(cfg) {
 SlabContext::~SlabContext() {
     cudaSetDevice(dev_);
     if (s_comp_) cudaStreamSynchronize(s_comp_);
+    if (s_prep_) cudaStreamSynchronize(s_prep_);
     if (s_copy_) cudaStreamSynchronize(s_copy_);
     if (s_d2h_) cudaStreamSynchronize(s_d2h_);
     for (auto e : ev_chunk_) cudaEventDestroy(e);
     for (auto e : ev_ready_) cudaEventDestroy(e);
     for (auto e : ev_free_) cudaEventDestroy(e);
+    for (auto e : ev_prep_) cudaEventDestroy(e);
     for (auto& p : launch_ev_) {
         cudaEventDestroy(p.first);
         cudaEventDestroy(p.second);
@@ -294,6 +311,7 @@ SlabContext::~SlabContext() {
     for (cudaEvent_t e : {ev_t0_, ev_t1_, ev_h0_, ev_h1_, ev_d0_, ev_d1_})
         if (e) cudaEventDestroy(e);
     if (s_comp_) cudaStreamDestroy(s_comp_);
+    if (s_prep_) cudaStreamDestroy(s_prep_);
     if (s_copy_) cudaStreamDestroy(s_copy_);
     if (s_d2h_) cudaStreamDestroy(s_d2h_);
     if (own_vol_ && d_vol_) cudaFree(d_vol_);
@@ -504,7 +522,7 @@ void SlabContext::choose_tile(const bpg::BatchArgs& b) {
     t.tw = tw;
     int ctas = (t.bx * t.by * t.bz == 4096) ? 3 : 4;
     if (t.bx == 32 && t.by == 16 && t.bz == 4) ctas = 5;
-    if ((t.bx == 32 && t.by == 32) || t.bx == 64) ctas = 2;
+    if ((t.bx == 32 && t.by == 32 && t.bz == 8) || t.bx == 64) ctas = 2;
     if (t.bx == 16 && t.by == 32) ctas = 4;
     if (const char* e = std::getenv("BP_CTAS")) ctas = std::max(1, std::atoi(e));
     t.th = bpg::ring_rows_for_shape(t, th, ctas);
@@ -577,10 +595,9 @@ void SlabContext::launch(const bpg::BatchArgs& b, int zc0, int zc1, bool final_p
 void SlabContext::launch_pending_front(bool final_pass) {
     Pending p = pending_.front();
     pending_.erase(pending_.begin());
-    check(cudaStreamWaitEvent(s_comp_, ev_ready_[(size_t)p.rg], 0), "wait");
+    prepare(p);
+    check(cudaStreamWaitEvent(s_comp_, p.ready, 0), "wait");
     mark_t0();
-    filter_pending(p);
-    expand_pending(p);
     p.b.load_volume = p.index > 0 ? 1 : 0;
     launch(p.b, 0, -1, final_pass);
     any_launch_ = true;
@@ -601,6 +618,7 @@ void SlabContext::flush() {
     choose_tile(cur_);
     check(cudaEventRecord(ev_ready_[(size_t)rg_], s_copy_), "event");
     pending_.push_back(Pending{cur_, rg_, batch_index_++, fr0_, fr1_});
+    prepare(pending_.back());
     rg_ = (rg_ + 1) % R_;
     nb_ = 0;
     while ((int)pending_.size() > tail_batches_) launch_pending_front();
@@ -620,13 +638,11 @@ void SlabContext::finish(float* host_volume, bp_gpu_stats* st) {
         std::vector<int> zb((size_t)C + 1);
         for (int c = 0; c <= C; ++c) zb[(size_t)c] = (int)((long long)nz_ * c / C / ts_.bz) * ts_.bz;
         zb[(size_t)C] = nz_;
-        for (const auto& p : pending_)
-            check(cudaStreamWaitEvent(s_comp_, ev_ready_[(size_t)p.rg], 0), "wait");
-        mark_t0();
         for (auto& p : pending_) {
-            filter_pending(p);
-            expand_pending(p);
+            prepare(p);
+            check(cudaStreamWaitEvent(s_comp_, p.ready, 0), "wait");
         }
+        mark_t0();
         for (int c = 0; c < C; ++c) {
             for (size_t i = 0; i < pending_.size(); ++i) {
                 auto p = pending_[i];
@@ -801,6 +817,9 @@ double SlabContext::time_resident(int iters, bp_gpu_stats* st) {
     reset_recon();
     check(cudaEventRecord(ev_t0_, s_comp_), "event");
     for (int it = 0; it < iters; ++it) {
+        // this pass's pair-ring expansions overwrite slots the previous pass read
+        check(cudaEventRecord(ev_free_[0], s_comp_), "event");
+        check(cudaStreamWaitEvent(s_prep_, ev_free_[0], 0), "wait");
         for (int k0 = 0; k0 < resident_; k0 += B_) {
             bpg::BatchArgs b{};
             b.nviews = std::min(B_, resident_ - k0);
@@ -810,7 +829,14 @@ double SlabContext::time_resident(int iters, bp_gpu_stats* st) {
                 b.slot[i] = k0 + i;
             }
             choose_tile(b);
-            expand(b);  // inside the timed region: part of every reconstruction
+            if (tiled_ && ts_.dy) {
+                // inside the timed region (part of every reconstruction), on the prep
+                // stream so batch k+1's expansion runs under batch k's kernel
+                const size_t gi = (size_t)(k0 / B_) % ev_prep_.size();
+                expand(b, s_prep_);
+                check(cudaEventRecord(ev_prep_[gi], s_prep_), "event");
+                check(cudaStreamWaitEvent(s_comp_, ev_prep_[gi], 0), "wait");
+            }
             launch(b, 0, -1, k0 + B_ >= resident_);
         }
     }

@@ -84,10 +84,12 @@ private:
         std::array<int, bpg::kMaxBatch> fr0, fr1;  // rows to filter per view (cfg_.filter)
         bool filtered = false;
         bool expanded = false;
+        cudaEvent_t ready = nullptr;  // the batch's inputs are final (uploaded + prepared)
     };
-    void filter_pending(Pending& p);
-    void expand_pending(Pending& p);
-    void expand(const bpg::BatchArgs& b);  // pair rows of the batch's slots (ts_.dy)
+    // FDK filter and pair-ring expansion of a batch on the low-priority prep stream,
+    // issued when the batch is queued so they run under earlier batches' kernels
+    void prepare(Pending& p);
+    void expand(const bpg::BatchArgs& b, cudaStream_t st);  // pair rows of the batch's slots
     void flush();
     void choose_tile(const bpg::BatchArgs& b);
     // launch over slab-local z range [zc0, zc1) (default: the whole slab)
@@ -112,7 +114,8 @@ private:
     unsigned long long* d_cnt_ = nullptr;
     float* h_stage_ = nullptr;  // pinned staging, slots views
     cudaStream_t s_comp_ = nullptr, s_copy_ = nullptr;
-    std::vector<cudaEvent_t> ev_ready_, ev_free_;
+    cudaStream_t s_prep_ = nullptr;  // low priority: filter + expansion of queued batches
+    std::vector<cudaEvent_t> ev_ready_, ev_free_, ev_prep_;
     std::vector<bool> used_;
     cudaEvent_t ev_t0_ = nullptr, ev_t1_ = nullptr, ev_h0_ = nullptr, ev_h1_ = nullptr,
                 ev_d0_ = nullptr, ev_d1_ = nullptr;

@@ -10,13 +10,16 @@ B = int(os.environ.get("AB_BATCH", "64"))
 reps = int(os.environ.get("AB_REPS", "5"))
 s = bp.Stack.baseline(n_views=496, isx=1248, isy=960)
 with bp.GpuContext(L, 1248, 960, device=0, strict=os.environ.get("AB_STRICT") == "1",
-                   view_batch=B, ring_batches=(496 + B - 1) // B) as c:
+                   view_batch=B, ring_batches=(496 + B - 1) // B,
+                   profile_launches=True) as c:
     c.upload_stack(s)
     c.time_resident(1)
-    v = []
+    v, kv = [], []
     for _ in range(reps):
         ms, st = c.time_resident(1)
         v.append(ms)
+        kv.append(st.kernel_ms)
 med = statistics.median(v)
+kmed = statistics.median(kv)
 print(f"{os.environ.get('AB_TAG', bp.LIB_PATH)}: L={L} B={B} median {med:.2f} ms -> "
-      f"{496 * L ** 3 / med / 1e6:.1f} GUP/s (tile {st.tile_w}x{st.tile_h}, fallback {st.fallback_pairs})")
+      f"{496 * L ** 3 / med / 1e6:.1f} GUP/s; backprojection kernels {kmed:.2f} ms (tile {st.tile_w}x{st.tile_h}, fallback {st.fallback_pairs})")
