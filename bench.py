@@ -291,23 +291,25 @@ def run_ours(args):
     clk.start()
     ms = 0.0
     launches = 0
+    prep_launches = 0
     kernel_ms = 0.0
     st = None
     for _ in range(args.steps):
         m, st = ctx.time_resident(1)
         ms += m + gather_ms()
         launches += int(st.launches)
+        prep_launches += int(st.prep_launches)
         kernel_ms += float(st.kernel_ms)
     clocks = clk.stop()
     if dist:
         t = torch.tensor([ms], dtype=torch.float64, device=ctrl)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
-        t = torch.tensor([launches], dtype=torch.float64, device=ctrl)
+        t = torch.tensor([launches + prep_launches], dtype=torch.float64, device=ctrl)
         dist.all_reduce(t, op=dist.ReduceOp.SUM)
         total_launches = int(t.item())
     else:
-        total_launches = launches
+        total_launches = launches + prep_launches
     nominal_step = n * L ** 3  # whole job, all ranks
     value = nominal_step * args.steps / (ms / 1e3) / 1e9
     per_launch_s = kernel_ms / 1e3 / max(1, launches)
@@ -425,6 +427,7 @@ def run_ours(args):
     # dominant kernel: tiled backprojection.  Algorithmic SMEM-load bytes per launch =
     # 16 B x visible updates per launch (4 fp32 texels per update).
     achieved = 16.0 * (visible / max(1e-9, launches_per_step)) / per_launch_s / 1e9
+    tex_bytes = 4.0 if args.strict else 8.0  # bytes per detector texel the kernel reads
     peak_nominal = SMEM_BYTES_PER_SM_CLK * N_SM * float(sm_max) * 1e6 / 1e9
     line = {
         "metric": METRIC, "value": value, "unit": "GUP/s", "n_gpus": world, "steps": args.steps,
@@ -433,7 +436,7 @@ def run_ours(args):
         "config": {"workload": f"{L}^3 x {n} views of 1248x960 (BASELINE config 3)", "l": L,
                    "views": n, "view_batch": args.batch, "e2e_view_batch": args.e2e_batch,
                    "arithmetic": "strict (bitwise reference)" if args.strict
-                   else "fast (FMA lerp, within north_star tolerance)",
+                   else "fast (pair-ring FMA lerp, within north_star tolerance)",
                    "l2": "no flush: inputs larger than L2 (2.38 GB stack + 512 MiB volume)",
                    "parallelism": f"z-slab x{world}" + (
                        "" if world == 1 else
@@ -441,6 +444,8 @@ def run_ours(args):
                        if fused else " + NCCL slab gather"),
                    "slab_bounds": [int(b) for b in bounds]},
         "gpu_launches": total_launches,
+        "gpu_launches_note": "backprojection launches + pair-ring expansion launches (one per view "
+                             "batch, bp_expand_kernel) inside the timed region",
         "visible_updates_per_step": visible_all,
         "gups_visible": visible_all * args.steps / (ms / 1e3) / 1e9,
         "kernel_ms_per_step": kernel_ms / args.steps,
@@ -455,12 +460,12 @@ def run_ours(args):
                                     "(MEASURED_PEAKS.json has no shared-memory figure)",
                      "frac_at_measured_clock": achieved / (peak_nominal * float(sm_mhz) / float(sm_max)),
                      "hbm_check": {
-                         "achieved": (8.0 * (z1 - z0) * L * L + 4.0 * isx * isy * n / max(1e-9, launches_per_step))
-                         / per_launch_s / 1e9,
+                         "achieved": (8.0 * (z1 - z0) * L * L + tex_bytes * isx * isy * n
+                                      / max(1e-9, launches_per_step)) / per_launch_s / 1e9,
                          "peak": peaks.get("hbm_gbs"), "unit": "GB/s",
                          "note": "algorithmic HBM bytes per launch (slab volume read + write, the launch's "
-                                 "views) / live mean launch time; ncu agrees (profiles/latest.json). HBM is "
-                                 "not the bound"},
+                                 "views: 8-byte pair-ring texels in fast mode, 4-byte raw in strict) / live "
+                                 "mean launch time; ncu: profiles/latest.json. HBM is not the bound"},
                      "binding_unit": {
                          "unit": "co-limit: LSU shared-memory wavefronts (1 per clk per SM) and FMA-pipe issue",
                          "util": prof.get("lsu_wavefronts_pct", 0.0) / 100.0,

@@ -76,7 +76,7 @@ class GpuStats(C.Structure):
                 ("h2d_bytes", C.c_uint64), ("d2h_bytes", C.c_uint64), ("tile_w", C.c_int),
                 ("tile_h", C.c_int), ("block_x", C.c_int), ("block_y", C.c_int),
                 ("block_z", C.c_int), ("device_updates_min", C.c_uint64),
-                ("device_updates_max", C.c_uint64)]
+                ("device_updates_max", C.c_uint64), ("prep_launches", C.c_uint64)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}

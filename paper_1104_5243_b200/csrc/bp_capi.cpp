@@ -599,6 +599,7 @@ int bp_reconstruct_ex(const bp_stack* s, uint32_t l, const bp_recon_ex* p, float
                 t.d2h_ms = std::max(t.d2h_ms, x.d2h_ms);
                 t.views = x.views;
                 t.launches += x.launches;
+                t.prep_launches += x.prep_launches;
                 t.nominal_updates += x.nominal_updates;
                 t.visible_updates += x.visible_updates;
                 t.tile_pairs += x.tile_pairs;

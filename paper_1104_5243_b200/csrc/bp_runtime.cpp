@@ -173,6 +173,7 @@ void SlabContext::prepare(Pending& p) {
         filt_->apply_batch(d_ring_, (long long)isy_ * pitch_, pitch_, p.b.nviews, p.b.slot,
                            p.fr0.data(), p.fr1.data(), s_prep_);
         filtered_views_ += (uint64_t)p.b.nviews;
+        ++prep_launches_;
         p.filtered = true;
     }
     if (expd) {
@@ -195,6 +196,7 @@ void SlabContext::expand(const bpg::BatchArgs& b, cudaStream_t st) {
     for (int i = 0; i < b.nviews; ++i) a.slot[i] = b.slot[i];
     check((cudaError_t)bpg::launch_expand(a, b.nviews, st), "pair ring expansion");
     expanded_views_ += (uint64_t)b.nviews;
+    ++prep_launches_;
 }
 
 void SlabContext::mark_t0() {
@@ -334,6 +336,7 @@ void SlabContext::reset_recon() {
     any_h2d_ = false;
     views_ = 0;
     launches_ = 0;
+    prep_launches_ = 0;
     h2d_bytes_ = 0;
     launch_ev_used_ = 0;
     wall_t0_ = 0.0;
@@ -448,7 +451,7 @@ void SlabContext::choose_tile(const bpg::BatchArgs& b) {
     };
     const auto sx = samples(nbx), sy = samples(nby), sz = samples(nbz);
     const int views[3] = {0, b.nviews / 2, b.nviews - 1};
-    int need_w = 0, need_h = 0;
+    int need_w = 0, need_h = 0, need_w2 = 0;  // need_w2: pair ring (2-texel aligned origin)
     for (int vi = 0; vi < 3; ++vi) {
         const float* A = b.A[views[vi]];
         for (int zi : sz)
@@ -478,12 +481,17 @@ void SlabContext::choose_tile(const bpg::BatchArgs& b) {
                     const int iv0 = (int)std::floor(vmin) - 1, iv1 = (int)std::floor(vmax) + 2;
                     if (iu1 < 0 || iu0 > isx_ - 1 || iv1 < 0 || iv0 > isy_ - 1) continue;
                     need_w = std::max(need_w, iu1 - iu0 + 1);
+                    need_w2 = std::max(need_w2, iu1 - (((int)std::floor(umin) - 1) & ~1) + 1);
                     need_h = std::max(need_h, iv1 - iv0 + 1);
                 }
     }
     // Row pitch of the SMEM tile == TMA box width.  Pitches == 20 (mod 32) floats
     // minimise bank conflicts of the 8x4 lane layout (tools/bank_sim.py).
-    int tw = round_up(std::max(need_w, 8) + 4, 4);
+    // The kernel checks every (block, view) footprint exactly and serves the rare one
+    // that does not fit through the exact global-memory fallback, so the pitch needs
+    // no guard beyond the TMA alignment.  (A guard that pushed the pair ring past its
+    // compile-time 152 forced a taller ring than two CTAs per SM hold: -25%, measured.)
+    int tw = t.dy ? round_up(std::max(need_w2, 8), 2) : round_up(std::max(need_w, 8) + 4, 4);
     const bool twc_ok = !std::getenv("BP_NO_TWC") && t.bx >= 32;
     // compile-time pitches (== 16 mod 32: immediate row offsets, low conflicts); the
     // smallest listed one that holds the footprint
@@ -525,7 +533,11 @@ void SlabContext::choose_tile(const bpg::BatchArgs& b) {
     if ((t.bx == 32 && t.by == 32 && t.bz == 8) || t.bx == 64) ctas = 2;
     if (t.bx == 16 && t.by == 32) ctas = 4;
     if (const char* e = std::getenv("BP_CTAS")) ctas = std::max(1, std::atoi(e));
-    t.th = bpg::ring_rows_for_shape(t, th, ctas);
+    // Prefer `ctas` CTAs per SM: the ring takes what their SMEM leaves, unless that
+    // cannot hold the largest sampled footprint (taller views use the fallback).
+    const int budget = bpg::ring_rows_for_shape(t, 0, ctas);
+    t.th = budget >= round_up(std::max(need_h, 8), 8) ? std::max(budget, std::min(th, budget))
+                                                        : bpg::ring_rows_for_shape(t, th, ctas);
     t.smem_bytes = bpg::smem_bytes_for(t);
     if (t.smem_bytes > 227 * 1024) throw bph::device_error("tile ring exceeds shared memory");
     char err[256];
@@ -710,6 +722,7 @@ void SlabContext::finish(float* host_volume, bp_gpu_stats* st) {
         st->kernel_ms = kms;
         st->views = views_;
         st->launches = launches_;
+        st->prep_launches = prep_launches_;
         st->nominal_updates = views_ * (uint64_t)nz_ * L_ * L_;
         st->visible_updates = cnt[3];
         st->tile_pairs = cnt[0];
@@ -859,6 +872,7 @@ double SlabContext::time_resident(int iters, bp_gpu_stats* st) {
         st->kernel_ms = kms;
         st->views = (uint64_t)resident_ * iters;
         st->launches = launches_;
+        st->prep_launches = prep_launches_;
         st->nominal_updates = st->views * (uint64_t)nz_ * L_ * L_;
         st->visible_updates = cnt[3];
         st->tile_pairs = cnt[0];

@@ -159,7 +159,7 @@ private:
     bool any_launch_ = false;
     bool t0_rec_ = false;
     bool any_h2d_ = false;
-    uint64_t views_ = 0, launches_ = 0, h2d_bytes_ = 0;
+    uint64_t views_ = 0, launches_ = 0, prep_launches_ = 0, h2d_bytes_ = 0;
     double wall_t0_ = 0.0;
 
     // resident views
