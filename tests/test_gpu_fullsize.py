@@ -97,3 +97,27 @@ def test_partial_blocks_at_large_odd_multiple_edge():
         ref = O.reconstruct_lines(px, mats, L, ys, zs)
         assert s1.fallback_pairs == 0
         assert bitwise_equal(got, ref), L
+
+
+@pytest.mark.parametrize("L,batch", [(512, 32), (512, 124), (520, 64)])
+def test_pair_ring_bitwise_equals_raw_tile(stack, L, batch, monkeypatch):
+    # the fast mode's pair ring (p, p_down - p) is a layout change only: the same IEEE
+    # subtraction as the raw-tile lerp, so whole volumes must agree bitwise (streamed
+    # path, row windows, deferred z-chunked tail included)
+    vols = {}
+    for name, flag in (("raw", "1"), ("pair", "0")):
+        monkeypatch.setenv("BP_NO_PAIR", flag)
+        c = bp.GpuContext(L, 1248, 960, device=0, strict=False, view_batch=batch)
+        c.backproject_stack(stack)
+        _, st = c.finish(readback=False)
+        vols[name] = (c, st)
+    monkeypatch.delenv("BP_NO_PAIR")
+    (raw, sr), (pair, sp) = vols["raw"], vols["pair"]
+    mx, mr, rms, nbit = pair.compare_with(raw)
+    assert nbit == 0, (mx, mr, rms)
+    assert sp.fallback_pairs == 0 and sr.fallback_pairs == 0
+    # one expansion per view batch; pitch 152 with the ring two CTAs per SM hold
+    assert sp.prep_launches == (496 + batch - 1) // batch and sr.prep_launches == 0
+    assert (sp.tile_w, sp.tile_h) == (152, 80)
+    raw.close()
+    pair.close()
