@@ -150,3 +150,26 @@ def test_filter_rejects_bad_geometry():
     assert e.value.code == bp.BP_EINVAL
     with pytest.raises(bp.BPError):
         bp.filter_views(np.zeros((1, 2, 9000), np.float32), SID, SDD, 1.0)
+
+
+@pytest.mark.gpu
+def test_in_pipeline_filter_pair_ring_fast_mode():
+    # the fast mode's pair ring is built on the prep stream from the FILTERED ring
+    # slots: at 512^3 (32x32x8 pair-ring kernel) the in-pipeline filter must still equal
+    # streaming prefiltered views, bitwise
+    raw, mats = baseline_small(n_views=21, shrink=1, filter=0)
+    geom = (SID, SDD, 0.32)
+    pre = bp.filter_views(raw, *geom)
+    n, isy, isx = raw.shape
+    kw = dict(view_batch=8, strict=False)
+    with bp.GpuContext(512, isx, isy, filter=geom, **kw) as ctx:
+        for k in range(n):
+            ctx.backproject(raw[k], mats[k])
+        got, st = ctx.finish()
+    with bp.GpuContext(512, isx, isy, **kw) as ctx:
+        for k in range(n):
+            ctx.backproject(pre[k], mats[k])
+        ref, st2 = ctx.finish()
+    assert st.tile_w == 152 and st.prep_launches == 2 * ((n + 7) // 8)  # filter + expansion
+    assert st2.prep_launches == (n + 7) // 8
+    assert bitwise_equal(got, ref)
