@@ -121,3 +121,17 @@ def test_pair_ring_bitwise_equals_raw_tile(stack, L, batch, monkeypatch):
     assert (sp.tile_w, sp.tile_h) == (152, 80)
     raw.close()
     pair.close()
+
+
+def test_pair_ring_virtual_slabs_row_windows_bitwise(stack):
+    # fast mode at 512^3 (pair ring) over 1, 2 and 4 work-balanced z-slabs on one GPU:
+    # each slab uploads only its detector-row window per view, its expansion then
+    # builds pair rows from a partly stale ring slot; the rows any voxel reads lie
+    # inside the window, so the volumes must agree bitwise
+    full, st1 = bp.reconstruct_ex(stack, 512, strict=False)
+    assert st1.tile_w == 152 and st1.fallback_pairs == 0
+    for G in (2, 4):
+        got, st = bp.reconstruct_ex(stack, 512, strict=False, virtual_slabs=G)
+        assert st.fallback_pairs == 0
+        assert st.h2d_bytes < G * st1.h2d_bytes  # windows: less than G full stacks
+        assert bitwise_equal(got, full), G
