@@ -64,7 +64,7 @@ class GpuConfig(C.Structure):
                 ("kernel", C.c_int), ("count_visible", C.c_int), ("profile_launches", C.c_int),
                 ("recip_mode", C.c_int), ("device_volume", C.c_void_p), ("filter", C.c_int),
                 ("sid_mm", C.c_double), ("sdd_mm", C.c_double), ("pitch_mm", C.c_double),
-                ("output_volume", C.c_void_p)]
+                ("output_volume", C.c_void_p), ("tail_batches", C.c_int)]
 
 
 class GpuStats(C.Structure):
@@ -493,7 +493,8 @@ class GpuContext:
     def __init__(self, l, isx, isy, *, offset=(0.0, 0.0, 0.0), device=-1, z_begin=0, z_end=0,
                  view_batch=32, ring_batches=0, strict=True, distance_weight=True,
                  row_windows=True, kernel=0, count_visible=False, profile_launches=False,
-                 recip_mode=0, device_volume=None, filter=None, output_volume=None):
+                 recip_mode=0, device_volume=None, filter=None, output_volume=None,
+                 tail_batches=-1):
         cfg = GpuConfig()
         lib().bp_gpu_config_init(C.byref(cfg))
         cfg.l, cfg.isx, cfg.isy = l, isx, isy
@@ -515,6 +516,7 @@ class GpuContext:
         cfg.profile_launches = int(profile_launches)
         cfg.recip_mode = recip_mode
         cfg.device_volume = device_volume
+        cfg.tail_batches = tail_batches
         self.l, self.isx, self.isy = l, isx, isy
         self.z_begin, self.z_end = z_begin, (z_end if z_end > 0 else l)
         h = C.c_void_p()

@@ -294,6 +294,7 @@ void bp_gpu_config_init(bp_gpu_config* c) {
     c->strict_mode = 1;
     c->distance_weight = 1;
     c->row_windows = 1;
+    c->tail_batches = -1;
 }
 
 int bp_gpu_load(const bp_gpu_config* cfg, bp_gpu_ctx** out) {

@@ -239,7 +239,7 @@ SlabContext::SlabContext(const bp_gpu_config& cfg) : cfg_(cfg) {
     R_ = cfg.ring_batches > 0 ? cfg.ring_batches : 8;
     // measured on B200 at 512^3 (tools: scratch e2e A/B): deferring 3 batches and
     // streaming 8 z-chunks back hides most of the 10 ms volume readback
-    tail_batches_ = std::max(0, std::min(R_ - 2, 3));
+    tail_batches_ = std::max(0, std::min(R_ - 2, cfg.tail_batches >= 0 ? cfg.tail_batches : 3));
     tail_chunks_ = 8;
     if (const char* e = std::getenv("BP_TAIL_BATCHES")) tail_batches_ = std::max(0, std::atoi(e));
     if (const char* e = std::getenv("BP_TAIL_CHUNKS")) tail_chunks_ = std::max(1, std::atoi(e));

@@ -135,3 +135,17 @@ def test_pair_ring_virtual_slabs_row_windows_bitwise(stack):
         assert st.fallback_pairs == 0
         assert st.h2d_bytes < G * st1.h2d_bytes  # windows: less than G full stacks
         assert bitwise_equal(got, full), G
+
+
+def test_tail_batches_config_is_result_invariant(stack):
+    # tail_batches only changes the launch order over z-chunks, never the per-voxel
+    # view order: volumes must be bitwise equal (0 = no deferred tail, as used by the
+    # two-context back-to-back e2e)
+    outs = []
+    for tb in (-1, 0, 1):
+        with bp.GpuContext(512, 1248, 960, device=0, strict=False, view_batch=32,
+                           tail_batches=tb) as c:
+            c.backproject_stack(stack)
+            vol, st = c.finish()
+            outs.append(vol)
+    assert bitwise_equal(outs[1], outs[0]) and bitwise_equal(outs[2], outs[0])
