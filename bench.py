@@ -396,7 +396,9 @@ def run_ours(args):
                 c.backproject_stack(stack)
                 c.finish(out=v.data)
         go = threading.Barrier(3)
-        nsteps = max(2, args.steps)
+        # an even count (both contexts equally busy), at least 12: the pipeline's fill
+        # (both first uploads share the link) and drain are amortised
+        nsteps = max(12, args.steps + (args.steps & 1))
 
         def worker(i, cnt):
             go.wait()
