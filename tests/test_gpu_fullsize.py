@@ -149,3 +149,25 @@ def test_tail_batches_config_is_result_invariant(stack):
             vol, st = c.finish()
             outs.append(vol)
     assert bitwise_equal(outs[1], outs[0]) and bitwise_equal(outs[2], outs[0])
+
+
+@pytest.mark.parametrize("isx,isy", [(1247, 957), (2048, 200)])
+def test_pair_ring_odd_and_wide_detectors(isx, isy, monkeypatch):
+    # pitch != isx (the pair ring shares the raw ring's padded pitch; TMA reads the
+    # padding as zeros), odd row counts, and a wide detector whose footprints need a
+    # runtime pitch above 152 -- pair ring vs raw tile, bitwise, at 512^3
+    s = bp.Stack.generate("spheres3", 12, isx, isy, 750.0, 1200.0, 0.32 * 1248.0 / isx)
+    vols = {}
+    for name, flag in (("raw", "1"), ("pair", "0")):
+        monkeypatch.setenv("BP_NO_PAIR", flag)
+        c = bp.GpuContext(512, isx, isy, device=0, strict=False, view_batch=5)
+        c.backproject_stack(s)
+        _, st = c.finish(readback=False)
+        vols[name] = (c, st)
+    monkeypatch.delenv("BP_NO_PAIR")
+    (raw, sr), (pair, sp) = vols["raw"], vols["pair"]
+    mx, mr, rms, nbit = pair.compare_with(raw)
+    assert nbit == 0, (mx, mr, rms, sp.tile_w, sp.fallback_pairs)
+    assert sp.prep_launches > 0 and mr > 0
+    raw.close()
+    pair.close()
