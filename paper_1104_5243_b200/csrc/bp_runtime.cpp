@@ -235,7 +235,7 @@ SlabContext::SlabContext(const bp_gpu_config& cfg) : cfg_(cfg) {
     isy_ = (int)cfg.isy;
     pitch_ = round_up(isx_, 4);  // TMA global strides must be multiples of 16 B
     B_ = cfg.view_batch > 0 ? cfg.view_batch : 32;
-    if (B_ > bpg::kMaxBatch) throw bph::config_error("view_batch exceeds 128");
+    if (B_ > bpg::kMaxBatch) throw bph::config_error("view_batch exceeds 256");
     R_ = cfg.ring_batches > 0 ? cfg.ring_batches : 8;
     // measured on B200 at 512^3 (tools: scratch e2e A/B): deferring 3 batches and
     // streaming 8 z-chunks back hides most of the 10 ms volume readback

@@ -470,14 +470,14 @@ def test_strict_bitwise_odd_and_wide_detectors(isx, isy, L):
 
 def test_module_config_errors():
     # bp_gpu_load validation: every rejected configuration returns BP_EINVAL with a message
-    bad = [dict(view_batch=129), dict(z_begin=10, z_end=5), dict(z_begin=-1, z_end=4),
+    bad = [dict(view_batch=257), dict(z_begin=10, z_end=5), dict(z_begin=-1, z_end=4),
            dict(recip_mode=7), dict(filter=(750.0, 0.0, 0.3))]
     for kw in bad:
         with pytest.raises(bp.BPError) as e:
             bp.GpuContext(32, 64, 48, **kw)
         assert e.value.code == bp.BP_EINVAL, kw
     # the largest batch is accepted and batch-invariant
-    px, mats = baseline_small(n_views=130, shrink=16)
+    px, mats = baseline_small(n_views=260, shrink=16)
     ref, _ = O.reconstruct(px, mats, 32)
-    got, _ = gpu_recon(px, mats, 32, view_batch=128)
+    got, _ = gpu_recon(px, mats, 32, view_batch=256)
     assert bitwise_equal(got, ref)
