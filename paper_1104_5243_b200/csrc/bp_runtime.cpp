@@ -172,7 +172,6 @@ void SlabContext::prepare(Pending& p) {
     if (filt) {
         filt_->apply_batch(d_ring_, (long long)isy_ * pitch_, pitch_, p.b.nviews, p.b.slot,
                            p.fr0.data(), p.fr1.data(), s_prep_);
-        filtered_views_ += (uint64_t)p.b.nviews;
         ++prep_launches_;
         p.filtered = true;
     }
@@ -195,7 +194,6 @@ void SlabContext::expand(const bpg::BatchArgs& b, cudaStream_t st) {
     a.pitchx = pitch_;
     for (int i = 0; i < b.nviews; ++i) a.slot[i] = b.slot[i];
     check((cudaError_t)bpg::launch_expand(a, b.nviews, st), "pair ring expansion");
-    expanded_views_ += (uint64_t)b.nviews;
     ++prep_launches_;
 }
 

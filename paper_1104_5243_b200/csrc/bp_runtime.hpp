@@ -124,7 +124,6 @@ private:
 
     // optional FDK preprocessing of every uploaded view (cfg_.filter)
     std::unique_ptr<RampFilter> filt_;
-    uint64_t filtered_views_ = 0;
     std::array<int, bpg::kMaxBatch> fr0_{}, fr1_{};  // current batch's filtered rows
 
     // tiled kernel
@@ -136,7 +135,6 @@ private:
     bool pair_ok_ = true;  // BP_NO_PAIR=1 keeps the raw-tile fast kernel (A/B)
     float2* d_ringx_ = nullptr;
     alignas(64) unsigned char tmapx_[128];
-    uint64_t expanded_views_ = 0;
 
     // deferred tail: the last tail_batches_ batches are held back and, when the
     // volume is read back, processed z-chunk-major so each finished chunk's D2H
