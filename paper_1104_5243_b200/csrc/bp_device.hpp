@@ -58,6 +58,7 @@ struct TileShape {
     int smem_bytes;
     int dy;                      // 1: fast-mode kernel over the pair ring (p, p_down - p),
                                  //    8-byte texels ("pair ring")
+    int xp;                      // x-pairs per thread; 0: the shape's default variant
 };
 
 // Picks the tiled-kernel variant for edge length L (returns false if the
