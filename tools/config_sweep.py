@@ -1,7 +1,8 @@
 """Single-B200 throughput for every BASELINE config (1-5), on the BASELINE stack.
 
 For each config it reports:
-- resident GUP/s: projections in HBM, device-event timing, nominal views·L³ per second;
+- resident GUP/s: projections in HBM, device-event timing, nominal views·L³ per second (248-view launches,
+  124 at 2048³);
 - visible GUP/s: clip_stats semantics;
 - e2e ms: pinned host stack in, host volume out, through the C ABI streaming call.
 
@@ -29,7 +30,7 @@ for L in Ls:
     with bp.GpuContext(L, 1248, 960, offset=off, count_visible=True, view_batch=32) as c:
         c.backproject_stack(s)
         _, vst = c.finish(readback=False)
-    B = 124
+    B = 124 if L >= 2048 else 248  # measured best resident launch size per L
     with bp.GpuContext(L, 1248, 960, offset=off, strict=False, view_batch=B,
                        ring_batches=(n + B - 1) // B) as c:
         c.upload_stack(s)
