@@ -171,3 +171,18 @@ def test_pair_ring_odd_and_wide_detectors(isx, isy, monkeypatch):
     assert sp.prep_launches > 0 and mr > 0
     raw.close()
     pair.close()
+
+
+def test_hw_rcp_tier_at_512_within_tolerance(stack):
+    # the opt-in hardware-reciprocal tier on the bench's kernel (pair ring, x-quads,
+    # 248-view batches) over the whole 512^3 volume, against strict (== reference)
+    strict, _ = _run(stack, 512, True)
+    with bp.GpuContext(512, 1248, 960, device=0, strict=False, view_batch=248,
+                       recip_mode=bp.BP_RECIP_HW_APPROX) as c:
+        c.backproject_stack(stack)
+        _, st = c.finish(readback=False)
+        assert st.tile_w == 152 and st.fallback_pairs == 0
+        mx, peak, rms, nbit = c.compare_with(strict)
+    strict.close()
+    assert peak > 0 and nbit > 0  # an approximation
+    assert mx / peak <= TOL_MAX and rms / peak <= TOL_RMS, (mx / peak, rms / peak)
