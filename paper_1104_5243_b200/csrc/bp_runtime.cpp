@@ -491,7 +491,8 @@ void SlabContext::choose_tile(const bpg::BatchArgs& b) {
                 }
     }
     // Row pitch of the SMEM tile == TMA box width.  Pitches == 20 (mod 32) floats
-    // minimise bank conflicts of the 8x4 lane layout (tools/bank_sim.py).
+    // minimise bank conflicts of the raw tile's 8x4 lane layout (tools/bank_sim.py),
+    // == 8 (mod 16) 8-byte texels those of the pair ring (tools/bank_sim64.py).
     // The kernel checks every (block, view) footprint exactly and serves the rare one
     // that does not fit through the exact global-memory fallback, so the pitch needs
     // no guard beyond the TMA alignment.  (A guard that pushed the pair ring past its
@@ -541,8 +542,7 @@ void SlabContext::choose_tile(const bpg::BatchArgs& b) {
     // Prefer `ctas` CTAs per SM: the ring takes what their SMEM leaves, unless that
     // cannot hold the largest sampled footprint (taller views use the fallback).
     const int budget = bpg::ring_rows_for_shape(t, 0, ctas);
-    t.th = budget >= round_up(std::max(need_h, 8), 8) ? std::max(budget, std::min(th, budget))
-                                                        : bpg::ring_rows_for_shape(t, th, ctas);
+    t.th = budget >= round_up(std::max(need_h, 8), 8) ? budget : bpg::ring_rows_for_shape(t, th, ctas);
     t.smem_bytes = bpg::smem_bytes_for(t);
     if (t.smem_bytes > 227 * 1024) throw bph::device_error("tile ring exceeds shared memory");
     char err[256];
@@ -600,8 +600,8 @@ void SlabContext::launch(const bpg::BatchArgs& b, int zc0, int zc1, bool final_p
     }
     int rc;
     if (tiled_)
-        rc = bpg::launch_tiled(ts_.dy ? tmapx_ : tmap_, s, b, ts_, cfg_.strict_mode != 0, cfg_.distance_weight != 0,
-                               cfg_.recip_mode == BP_RECIP_HW_APPROX, s_comp_);
+        rc = bpg::launch_tiled(ts_.dy ? tmapx_ : tmap_, s, b, ts_, cfg_.strict_mode != 0,
+                               cfg_.distance_weight != 0, cfg_.recip_mode == BP_RECIP_HW_APPROX, s_comp_);
     else
         rc = bpg::launch_simple(s, b, cfg_.distance_weight != 0, cfg_.recip_mode, s_comp_);
     check((cudaError_t)rc, "backprojection kernel launch");
