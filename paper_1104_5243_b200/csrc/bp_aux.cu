@@ -220,6 +220,43 @@ __global__ void __launch_bounds__(128) bp_expand_kernel(const __grid_constant__ 
     }
 }
 
+// The same expansion as a small grid (one 128-thread, 32-register block per SM) that
+// fits beside two resident backprojection CTAs (2 x 320 threads x 96 registers leave
+// exactly 4096 registers and ~2 KB of shared memory per SM): launched just BEFORE a
+// batch's backprojection, it builds the next batch's pair rows underneath it.
+__global__ void __launch_bounds__(128, 16) bp_expand_small_kernel(const __grid_constant__ ExpandArgs a,
+                                                                  int nviews) {
+    const int rows = a.isy + 1, n4 = a.pitch / 4;
+    const long long units = (long long)nviews * rows;
+    for (long long u = blockIdx.x; u < units; u += gridDim.x) {
+        const int e = (int)(u % rows);
+        const size_t slot = (size_t)a.slot[u / rows];
+        const float* img = a.ring + slot * a.isy * a.pitch;
+        const float4* up = reinterpret_cast<const float4*>(img + (size_t)(e - 1) * a.pitch);
+        const float4* dn = reinterpret_cast<const float4*>(img + (size_t)e * a.pitch);
+        float4* out = reinterpret_cast<float4*>(a.ringx + (slot * rows + e) * a.pitchx);
+        for (int c = threadIdx.x; c < n4; c += blockDim.x) {
+            const float4 zero = make_float4(0.f, 0.f, 0.f, 0.f);
+            const float4 p = e > 0 ? __ldg(up + c) : zero;
+            const float4 q = e < a.isy ? __ldg(dn + c) : zero;
+            out[2 * c] = make_float4(p.x, __fsub_rn(q.x, p.x), p.y, __fsub_rn(q.y, p.y));
+            out[2 * c + 1] = make_float4(p.z, __fsub_rn(q.z, p.z), p.w, __fsub_rn(q.w, p.w));
+        }
+    }
+}
+
+int launch_expand_small(const ExpandArgs& a, int n, int blocks, void* stream) {
+    if (n < 1) return 0;
+    if (a.pitch % 4 || a.pitchx < a.pitch) return (int)cudaErrorInvalidValue;
+    static const bool carve = [] {
+        return cudaFuncSetAttribute(bp_expand_small_kernel,
+                                    cudaFuncAttributePreferredSharedMemoryCarveout, 100) == cudaSuccess;
+    }();
+    (void)carve;
+    bp_expand_small_kernel<<<blocks, 128, 0, (cudaStream_t)stream>>>(a, n);
+    return (int)cudaGetLastError();
+}
+
 int launch_expand(const ExpandArgs& a, int n, void* stream) {
     if (n < 1) return 0;
     if (a.pitch % 4 || a.pitchx < a.pitch) return (int)cudaErrorInvalidValue;

@@ -83,6 +83,9 @@ struct ExpandArgs {
     int slot[kMaxBatch];
 };
 int launch_expand(const ExpandArgs& a, int n, void* stream);
+// Same result from `blocks` co-resident 128-thread blocks (one per SM), for running
+// under a backprojection launch.
+int launch_expand_small(const ExpandArgs& a, int n, int blocks, void* stream);
 
 // True when a pair-ring (dy) variant exists for this block shape.
 bool has_pair_variant(const TileShape& ts);

@@ -183,7 +183,7 @@ void SlabContext::prepare(Pending& p) {
     p.ready = ev_prep_[(size_t)p.rg];
 }
 
-void SlabContext::expand(const bpg::BatchArgs& b, cudaStream_t st) {
+void SlabContext::expand(const bpg::BatchArgs& b, cudaStream_t st, bool small) {
     if (!tiled_ || !ts_.dy) return;
     bpg::ExpandArgs a{};
     a.ring = d_ring_;
@@ -193,7 +193,9 @@ void SlabContext::expand(const bpg::BatchArgs& b, cudaStream_t st) {
     a.pitch = pitch_;
     a.pitchx = pitch_;
     for (int i = 0; i < b.nviews; ++i) a.slot[i] = b.slot[i];
-    check((cudaError_t)bpg::launch_expand(a, b.nviews, st), "pair ring expansion");
+    check((cudaError_t)(small ? bpg::launch_expand_small(a, b.nviews, num_sms_, st)
+                              : bpg::launch_expand(a, b.nviews, st)),
+          "pair ring expansion");
     ++prep_launches_;
 }
 
@@ -271,8 +273,14 @@ SlabContext::SlabContext(const bp_gpu_config& cfg) : cfg_(cfg) {
     check(cudaMemset(d_cnt_, 0, 8 * sizeof(unsigned long long)), "cudaMemset(counters)");
     int prio_lo = 0, prio_hi = 0;
     check(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi), "stream priorities");
-    check(cudaStreamCreateWithPriority(&s_comp_, cudaStreamNonBlocking, prio_hi), "stream");
+    // s_aux_ outranks s_comp_ so its small grid is dispatched ahead of a backprojection
+    // grid that becomes ready at the same time
+    const int prio_comp = prio_hi < prio_lo ? prio_hi + 1 : prio_hi;
+    check(cudaStreamCreateWithPriority(&s_comp_, cudaStreamNonBlocking, prio_comp), "stream");
+    check(cudaStreamCreateWithPriority(&s_aux_, cudaStreamNonBlocking, prio_hi), "stream");
     check(cudaStreamCreateWithPriority(&s_prep_, cudaStreamNonBlocking, prio_lo), "stream");
+    check(cudaDeviceGetAttribute(&num_sms_, cudaDevAttrMultiProcessorCount, dev_), "SM count");
+    if (const char* e = std::getenv("BP_NO_OVERLAP_EXPAND")) overlap_expand_ = std::atoi(e) == 0;
     check(cudaStreamCreateWithFlags(&s_copy_, cudaStreamNonBlocking), "stream");
     check(cudaStreamCreateWithFlags(&s_d2h_, cudaStreamNonBlocking), "stream");
     ev_chunk_.resize((size_t)tail_chunks_);
@@ -298,6 +306,7 @@ SlabContext::~SlabContext() {
     cudaSetDevice(dev_);
     if (s_comp_) cudaStreamSynchronize(s_comp_);
     if (s_prep_) cudaStreamSynchronize(s_prep_);
+    if (s_aux_) cudaStreamSynchronize(s_aux_);
     if (s_copy_) cudaStreamSynchronize(s_copy_);
     if (s_d2h_) cudaStreamSynchronize(s_d2h_);
     for (auto e : ev_chunk_) cudaEventDestroy(e);
@@ -312,6 +321,7 @@ SlabContext::~SlabContext() {
         if (e) cudaEventDestroy(e);
     if (s_comp_) cudaStreamDestroy(s_comp_);
     if (s_prep_) cudaStreamDestroy(s_prep_);
+    if (s_aux_) cudaStreamDestroy(s_aux_);
     if (s_copy_) cudaStreamDestroy(s_copy_);
     if (s_d2h_) cudaStreamDestroy(s_d2h_);
     if (own_vol_ && d_vol_) cudaFree(d_vol_);
@@ -848,12 +858,25 @@ double SlabContext::time_resident(int iters, bp_gpu_stats* st) {
             }
             choose_tile(b);
             if (tiled_ && ts_.dy) {
-                // inside the timed region (part of every reconstruction), on the prep
-                // stream so batch k+1's expansion runs under batch k's kernel
+                // Inside the timed region (part of every reconstruction).  The first
+                // batch's pair rows come from the full-grid expansion; each later
+                // batch's from the small grid launched just before the previous
+                // batch's kernel, which it runs under (co-resident, higher priority)
                 const size_t gi = (size_t)(k0 / B_) % ev_prep_.size();
-                expand(b, s_prep_);
-                check(cudaEventRecord(ev_prep_[gi], s_prep_), "event");
+                if (k0 == 0 || !overlap_expand_) {
+                    expand(b, s_prep_);
+                    check(cudaEventRecord(ev_prep_[gi], s_prep_), "event");
+                }
                 check(cudaStreamWaitEvent(s_comp_, ev_prep_[gi], 0), "wait");
+                if (overlap_expand_ && k0 + B_ < resident_) {
+                    bpg::BatchArgs nb{};
+                    nb.nviews = std::min(B_, resident_ - (k0 + B_));
+                    for (int i = 0; i < nb.nviews; ++i) nb.slot[i] = k0 + B_ + i;
+                    const size_t gn = (size_t)((k0 + B_) / B_) % ev_prep_.size();
+                    check(cudaStreamWaitEvent(s_aux_, ev_prep_[gi], 0), "wait");
+                    expand(nb, s_aux_, true);
+                    check(cudaEventRecord(ev_prep_[gn], s_aux_), "event");
+                }
             }
             launch(b, 0, -1, k0 + B_ >= resident_);
         }

@@ -89,7 +89,8 @@ private:
     // FDK filter and pair-ring expansion of a batch on the low-priority prep stream,
     // issued when the batch is queued so they run under earlier batches' kernels
     void prepare(Pending& p);
-    void expand(const bpg::BatchArgs& b, cudaStream_t st);  // pair rows of the batch's slots
+    // pair rows of the batch's slots; small: the co-resident small grid (under a kernel)
+    void expand(const bpg::BatchArgs& b, cudaStream_t st, bool small = false);
     void flush();
     void choose_tile(const bpg::BatchArgs& b);
     // launch over slab-local z range [zc0, zc1) (default: the whole slab)
@@ -115,6 +116,9 @@ private:
     float* h_stage_ = nullptr;  // pinned staging, slots views
     cudaStream_t s_comp_ = nullptr, s_copy_ = nullptr;
     cudaStream_t s_prep_ = nullptr;  // low priority: filter + expansion of queued batches
+    cudaStream_t s_aux_ = nullptr;   // highest priority: expansion under a running kernel
+    bool overlap_expand_ = true;     // BP_NO_OVERLAP_EXPAND=1: resident expansions in series
+    int num_sms_ = 0;
     std::vector<cudaEvent_t> ev_ready_, ev_free_, ev_prep_;
     std::vector<bool> used_;
     cudaEvent_t ev_t0_ = nullptr, ev_t1_ = nullptr, ev_h0_ = nullptr, ev_h1_ = nullptr,
