@@ -205,3 +205,36 @@ def test_resident_bench_path_equals_streaming_at_512(stack, batch):
                 assert st.prep_launches == (496 + batch - 1) // batch
                 mx, mr, rms, nbit = c.compare_with(ref)
                 assert nbit == 0, (mx, mr, rms)
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_pair_ring_random_geometry_fuzz(seed, monkeypatch):
+    # random single-view geometries (test_support.hpp:32-45) stacked into one scan,
+    # random detector sizes, grid offsets and view batches, at edge lengths that take the
+    # pair-ring kernels (x-quads below 1024, two y-rows at 1024): fast mode with the pair
+    # ring is bitwise the raw-tile fast kernel
+    from tests.helpers import random_image, random_matrix
+    rng = np.random.default_rng(7000 + seed)
+    isx, isy = int(rng.integers(100, 1400)), int(rng.integers(60, 1000))
+    n = int(rng.integers(3, 12))
+    mats = np.stack([random_matrix(int(rng.integers(0, 1 << 30)), isx, isy) for _ in range(n)])
+    px = np.stack([random_image(isx, isy, int(rng.integers(0, 1 << 30)), -1.0, 2.0) for _ in range(n)])
+    s = bp.Stack.from_arrays(px, mats)
+    L = int(rng.choice([512, 520, 1024]))
+    off = tuple(float(v) for v in rng.uniform(-40, 40, size=3))
+    batch = int(rng.integers(1, 9))
+    ctx = {}
+    for name, flag in (("raw", "1"), ("pair", "0")):
+        monkeypatch.setenv("BP_NO_PAIR", flag)
+        c = bp.GpuContext(L, isx, isy, device=0, offset=off, strict=False, view_batch=batch)
+        c.backproject_stack(s)
+        _, st = c.finish(readback=False)
+        ctx[name] = (c, st)
+    monkeypatch.delenv("BP_NO_PAIR")
+    (raw, sr), (pair, sp) = ctx["raw"], ctx["pair"]
+    try:
+        mx, mr, rms, nbit = pair.compare_with(raw)
+        assert nbit == 0, (L, isx, isy, n, mx, mr, rms, sp.tile_w, sp.fallback_pairs)
+    finally:
+        raw.close()
+        pair.close()
