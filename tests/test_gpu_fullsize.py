@@ -190,9 +190,10 @@ def test_hw_rcp_tier_at_512_within_tolerance(stack):
 
 @pytest.mark.parametrize("batch", [248, 166])
 def test_resident_bench_path_equals_streaming_at_512(stack, batch):
-    # the bench's `value` path: resident views, 248-view launches, the first batch's
-    # pair rows from the full-grid expansion and every later batch's from the small grid
-    # running under the previous launch -- bitwise equal to the streamed reconstruction
+    # the bench's `value` path: resident views, a quarter-size first batch then 248-view
+    # launches, the first batch's pair rows from the full-grid expansion and every later
+    # batch's from the small grid running under the previous launch -- bitwise equal to
+    # the streamed reconstruction
     with bp.GpuContext(512, 1248, 960, device=0, strict=False, view_batch=32) as ref:
         ref.backproject_stack(stack)
         ref.finish(readback=False)
@@ -202,7 +203,8 @@ def test_resident_bench_path_equals_streaming_at_512(stack, batch):
             for _ in range(2):  # twice: the second pass rewrites the pair ring it read
                 ms, st = c.time_resident(1)
                 assert st.fallback_pairs == 0 and st.tile_w == 152
-                assert st.prep_launches == (496 + batch - 1) // batch
+                first = batch // 4  # quarter-size first batch (its expansion runs in series)
+                assert st.prep_launches == 1 + (496 - first + batch - 1) // batch
                 mx, mr, rms, nbit = c.compare_with(ref)
                 assert nbit == 0, (mx, mr, rms)
 
