@@ -1,0 +1,45 @@
+"""Projected multi-GPU scaling from per-slab measurements on ONE B200 (not a scaling
+measurement: no NVLink, no concurrent PCIe links).
+
+For G = 1, 2, 4, 8 the volume is split into the work-balanced z-slabs every rank would
+build (bp_partition_slabs); each slab is reconstructed on this GPU:
+- resident: views in HBM, device-event time of the slab's kernels (bench `value` path);
+- e2e: the slab's streamed reconstruction through the C ABI, uploading only the slab's
+  detector-row window per view and reading back only its slab.
+A G-GPU run takes as long as its slowest slab (each GPU has its own PCIe link on an
+8 x B200 box), plus the fused slab gather (the final kernel stores into rank 0's volume
+over NVLink; not modelled). Efficiency = T1 / (G * max_g T_g).
+Usage: python tools/scaling_projection.py [L=1024]"""
+import sys, time
+sys.path.insert(0, ".")
+import paper_1104_5243_b200 as bp
+
+L = int(sys.argv[1]) if len(sys.argv) > 1 else 1024
+s = bp.Stack.baseline(n_views=496, isx=1248, isy=960)
+px, mats = s.pixels, s.matrices
+n = 496
+B = 248 if L < 2048 else 124
+res, e2e = {}, {}
+print(f"| G | slab bounds | slowest slab, resident ms | projected resident efficiency | slowest slab, e2e ms | projected e2e efficiency |")
+print("|---|---|---|---|---|---|")
+for G in (1, 2, 4, 8):
+    bounds = [int(b) for b in bp.partition_slabs(mats, 1248, 960, L, G)] if G > 1 else [0, L]
+    tr, te = [], []
+    for g in range(G):
+        z0, z1 = bounds[g], bounds[g + 1]
+        with bp.GpuContext(L, 1248, 960, device=0, z_begin=z0, z_end=z1, strict=False, view_batch=B,
+                           ring_batches=(n + B - 1) // B) as c:
+            c.upload_stack(s)
+            c.time_resident(1)
+            tr.append(min(c.time_resident(1)[0] for _ in range(2)))
+        out = bp.Volume.create(L).data[z0:z1]
+        with bp.GpuContext(L, 1248, 960, device=0, z_begin=z0, z_end=z1, strict=False, view_batch=32) as c:
+            c.backproject_stack(s)
+            c.finish(out=out)
+            t0 = time.perf_counter()
+            c.backproject_stack(s)
+            c.finish(out=out)
+            te.append((time.perf_counter() - t0) * 1e3)
+    res[G], e2e[G] = max(tr), max(te)
+    print(f"| {G} | {bounds} | {res[G]:.1f} | {res[1] / (G * res[G]):.3f} | {e2e[G]:.1f} | "
+          f"{e2e[1] / (G * e2e[G]):.3f} |", flush=True)
