@@ -20,6 +20,7 @@ px, mats = s.pixels, s.matrices
 n = 496
 B = 248 if L < 2048 else 124
 res, e2e = {}, {}
+host = bp.Volume.create(L)  # one pinned host volume; each slab reads back into its part
 print(f"| G | slab bounds | slowest slab, resident ms | projected resident efficiency | slowest slab, e2e ms | projected e2e efficiency |")
 print("|---|---|---|---|---|---|")
 for G in (1, 2, 4, 8):
@@ -32,14 +33,17 @@ for G in (1, 2, 4, 8):
             c.upload_stack(s)
             c.time_resident(1)
             tr.append(min(c.time_resident(1)[0] for _ in range(2)))
-        out = bp.Volume.create(L).data[z0:z1]
+        out = host.data[z0:z1]
         with bp.GpuContext(L, 1248, 960, device=0, z_begin=z0, z_end=z1, strict=False, view_batch=32) as c:
             c.backproject_stack(s)
             c.finish(out=out)
-            t0 = time.perf_counter()
-            c.backproject_stack(s)
-            c.finish(out=out)
-            te.append((time.perf_counter() - t0) * 1e3)
+            best = 1e30
+            for _ in range(2):
+                t0 = time.perf_counter()
+                c.backproject_stack(s)
+                c.finish(out=out)
+                best = min(best, (time.perf_counter() - t0) * 1e3)
+            te.append(best)
     res[G], e2e[G] = max(tr), max(te)
     print(f"| {G} | {bounds} | {res[G]:.1f} | {res[1] / (G * res[G]):.3f} | {e2e[G]:.1f} | "
           f"{e2e[1] / (G * e2e[G]):.3f} |", flush=True)
