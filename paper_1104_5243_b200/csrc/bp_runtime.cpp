@@ -238,8 +238,12 @@ SlabContext::SlabContext(const bp_gpu_config& cfg) : cfg_(cfg) {
     if (B_ > bpg::kMaxBatch) throw bph::config_error("view_batch exceeds 256");
     R_ = cfg.ring_batches > 0 ? cfg.ring_batches : 8;
     // measured on B200 at 512^3 (tools: scratch e2e A/B): deferring 3 batches and
-    // streaming 8 z-chunks back hides most of the 10 ms volume readback
-    tail_batches_ = std::max(0, std::min(R_ - 2, cfg.tail_batches >= 0 ? cfg.tail_batches : 3));
+    // streaming 8 z-chunks back hides most of the 10 ms volume readback.  A z-slab of a
+    // multi-GPU split uploads only its row windows, so its upload ends well before its
+    // compute and 5 deferred batches hide more of its readback (1024^3, outer slab of 8:
+    // 60.6 -> 55.7 ms; the whole volume at 512^3 prefers 3: 53.5 vs 59.2 ms)
+    const int tail_default = (z1_ - z0_ < L_) ? 5 : 3;
+    tail_batches_ = std::max(0, std::min(R_ - 2, cfg.tail_batches >= 0 ? cfg.tail_batches : tail_default));
     tail_chunks_ = 8;
     if (const char* e = std::getenv("BP_TAIL_BATCHES")) tail_batches_ = std::max(0, std::atoi(e));
     if (const char* e = std::getenv("BP_TAIL_CHUNKS")) tail_chunks_ = std::max(1, std::atoi(e));
