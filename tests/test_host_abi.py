@@ -169,3 +169,28 @@ def test_row_window_is_conservative():
         assert bitwise_equal(full, win), (z0, z1)
         if z1 - z0 <= 12:
             assert np.mean(rows) < isy
+
+
+def test_ctypes_mirrors_match_the_c_headers(tmp_path):
+    # the Python mirrors of bp_gpu_config / bp_gpu_stats must match include/bp_gpu.h
+    # byte for byte (fields are appended over time: tail_batches, prep_launches)
+    import ctypes as C
+    import shutil
+    import subprocess
+    if not shutil.which("gcc"):
+        pytest.skip("no C compiler")
+    src = tmp_path / "sizes.c"
+    inc = str(__import__("pathlib").Path(__file__).resolve().parents[1] / "include")
+    src.write_text(
+        '#include <stddef.h>\n#include <stdio.h>\n#include "bp_gpu.h"\n'
+        'int main(void) {\n'
+        '  printf("%zu %zu %zu %zu %zu\\n", sizeof(bp_gpu_config), sizeof(bp_gpu_stats),\n'
+        '         offsetof(bp_gpu_config, tail_batches), offsetof(bp_gpu_stats, prep_launches),\n'
+        '         offsetof(bp_gpu_config, output_volume));\n  return 0;\n}\n')
+    exe = tmp_path / "sizes"
+    subprocess.run(["gcc", "-I", inc, str(src), "-o", str(exe)], check=True)
+    got = [int(v) for v in subprocess.run([str(exe)], capture_output=True, text=True,
+                                          check=True).stdout.split()]
+    want = [C.sizeof(bp.GpuConfig), C.sizeof(bp.GpuStats), bp.GpuConfig.tail_batches.offset,
+            bp.GpuStats.prep_launches.offset, bp.GpuConfig.output_volume.offset]
+    assert got == want, (got, want)
