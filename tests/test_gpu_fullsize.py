@@ -188,16 +188,16 @@ def test_hw_rcp_tier_at_512_within_tolerance(stack):
     assert mx / peak <= TOL_MAX and rms / peak <= TOL_RMS, (mx / peak, rms / peak)
 
 
-@pytest.mark.parametrize("batch", [248, 166])
-def test_resident_bench_path_equals_streaming_at_512(stack, batch):
+@pytest.mark.parametrize("L,batch", [(512, 248), (512, 166), (1024, 248)])
+def test_resident_bench_path_equals_streaming(stack, L, batch):
     # the bench's `value` path: resident views, a quarter-size first batch then 248-view
     # launches, the first batch's pair rows from the full-grid expansion and every later
     # batch's from the small grid running under the previous launch -- bitwise equal to
     # the streamed reconstruction
-    with bp.GpuContext(512, 1248, 960, device=0, strict=False, view_batch=32) as ref:
+    with bp.GpuContext(L, 1248, 960, device=0, strict=False, view_batch=32) as ref:
         ref.backproject_stack(stack)
         ref.finish(readback=False)
-        with bp.GpuContext(512, 1248, 960, device=0, strict=False, view_batch=batch,
+        with bp.GpuContext(L, 1248, 960, device=0, strict=False, view_batch=batch,
                            ring_batches=(496 + batch - 1) // batch) as c:
             c.upload_stack(stack)
             for _ in range(2):  # twice: the second pass rewrites the pair ring it read
