@@ -20,6 +20,7 @@ Inputs are seeded synthetic (BASELINE.json configs).
 from __future__ import annotations
 
 import argparse
+import ctypes
 import json
 import os
 import subprocess
@@ -34,6 +35,7 @@ import numpy as np  # noqa: E402
 
 METRIC = "GUP/s (voxel updates/s) for 512^3x496-view backprojection"
 SMEM_BYTES_PER_SM_CLK = 128.0
+CONFIG_OF_L = {128: 1, 256: 2, 512: 3, 1024: 4, 2048: 5}
 N_SM = 148
 
 
@@ -114,64 +116,167 @@ def make_stack(args):
 
 
 # ---------------------------------------------------------------------------
-# reference arm: the reference's own CPU implementation (oracle/_ref)
+# reference arm: the reference's own CPU implementation (oracle/_ref: the unmodified
+# reference sources, compiled by oracle/Makefile), driven through ITS public C ABI
+# (bp_stack_read + bp_reconstruct, proj/include/backproject.h).  The process never
+# loads this repository's library: the seeded BASELINE stack is written to a BPST file
+# by a separate process (`bench.py --write-stack`), and the reference's own reader
+# loads it.
 
-def cpu_reference_run(px, mats, L, sample_views, threads):
-    """bp::reconstruct of the reference (lanes 8, block_b 8, clip on, exact), BASELINE.md 3."""
-    from oracle import oracle as O
-    if O.ref() is not None:
-        sub_px, sub_m = px[:sample_views], mats[:sample_views]
-        t0 = time.time()
-        vol, st = O.ref_reconstruct(sub_px, sub_m, L, threads=threads, lanes=8, block_b=8,
-                                    clip=True)
-        wall = time.time() - t0
-        nominal = sample_views * L ** 3
-        return {"kind": "reference", "value": nominal / wall / 1e9, "wall_s": wall,
-                "timed_region_s": st["seconds"], "performed_updates": st["voxel_updates"],
-                "nominal_updates": nominal}
-    # oracle port (the reference could not be built here)
-    sub_px, sub_m = px[:sample_views], mats[:sample_views]
-    t0 = time.time()
-    O.reconstruct(sub_px, sub_m, L, threads=threads)
-    wall = time.time() - t0
-    nominal = sample_views * L ** 3
-    return {"kind": "port", "value": nominal / wall / 1e9, "wall_s": wall,
-            "nominal_updates": nominal}
+class RefReconParams(ctypes.Structure):
+    """bp_recon_params, proj/include/backproject.h:60-73."""
+    _fields_ = [("l", ctypes.c_uint32), ("threads", ctypes.c_int), ("chunk", ctypes.c_int),
+                ("block_b", ctypes.c_int), ("lanes", ctypes.c_int), ("recip_mode", ctypes.c_int),
+                ("extract", ctypes.c_int), ("strict_mode", ctypes.c_int),
+                ("distance_weight", ctypes.c_int), ("clip", ctypes.c_int),
+                ("numa_domains", ctypes.c_int), ("clip_cache", ctypes.c_char_p)]
+
+
+class RefReconStats(ctypes.Structure):
+    """bp_recon_stats, proj/include/backproject.h:75-84."""
+    _fields_ = [("seconds", ctypes.c_double), ("voxel_updates", ctypes.c_uint64),
+                ("gups", ctypes.c_double), ("gflops", ctypes.c_double),
+                ("writeback_stores", ctypes.c_uint64), ("bytes_copied", ctypes.c_uint64),
+                ("clip_reduction", ctypes.c_double), ("thread_updates_min", ctypes.c_uint64),
+                ("thread_updates_max", ctypes.c_uint64)]
+
+
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def stack_file(views: int, seed: int, sample: int) -> str:
+    """BPST file of the first `sample` views of the seeded `views`-view BASELINE stack,
+    written by a separate process (this process must not load the repo's library)."""
+    d = os.environ.get("BP_BENCH_TMP", "/tmp")
+    path = os.path.join(d, f"bp_baseline_s{seed}_v{views}_n{sample}.bpst")
+    want = 16 + sample * (96 + 4 * 1248 * 960)  # BPST: magic, isx, isy, count, matrices, pixels
+    if not (os.path.exists(path) and os.path.getsize(path) >= want):
+        subprocess.run([sys.executable, os.path.abspath(__file__), "--write-stack", path,
+                        "--views", str(views), "--seed", str(seed), "--sample-views", str(sample)],
+                       check=True)
+    return path
+
+
+def write_stack(args):
+    import paper_1104_5243_b200 as bp
+    s = bp.Stack.baseline(n_views=args.views, isx=1248, isy=960, seed=args.seed)
+    n = args.sample_views or args.views
+    if n < args.views:
+        s = bp.Stack.from_arrays(s.pixels[:n], s.matrices[:n])
+    tmp = args.write_stack + ".part"
+    s.write(tmp)
+    os.replace(tmp, args.write_stack)
+    return 0
+
+
+def reference_reconstructions(path, L, steps, warmup, threads):
+    """Times `steps` complete bp_reconstruct calls of the reference (lanes 8, block_b 8,
+    clip on with its own clip_cache, exact reciprocal: BASELINE.md section 3) on the BPST
+    stack at `path`.  Returns (per-step wall seconds, last stats, views)."""
+    from oracle import oracle as O  # ctypes loader of oracle/_ref only
+    R = O.ref()
+    if R is None:
+        raise RuntimeError("oracle/_ref (the reference library) is not built")
+    R.bp_stack_read.argtypes = [ctypes.c_char_p, ctypes.POINTER(ctypes.c_void_p)]
+    R.bp_stack_dims.argtypes = [ctypes.c_void_p, ctypes.POINTER(ctypes.c_uint32),
+                                ctypes.POINTER(ctypes.c_uint32), ctypes.POINTER(ctypes.c_uint32)]
+    R.bp_stack_free.argtypes = [ctypes.c_void_p]
+    R.bp_reconstruct.argtypes = [ctypes.c_void_p, ctypes.POINTER(RefReconParams),
+                                 ctypes.POINTER(ctypes.c_void_p), ctypes.POINTER(RefReconStats)]
+    R.bp_volume_free.argtypes = [ctypes.c_void_p]
+    R.bp_last_error.restype = ctypes.c_char_p
+    h = ctypes.c_void_p()
+    if R.bp_stack_read(path.encode(), ctypes.byref(h)) != 0:
+        raise RuntimeError(R.bp_last_error().decode())
+    isx, isy, cnt = ctypes.c_uint32(), ctypes.c_uint32(), ctypes.c_uint32()
+    R.bp_stack_dims(h, ctypes.byref(isx), ctypes.byref(isy), ctypes.byref(cnt))
+    cache = path + f".L{L}.bpct"
+    p = RefReconParams(l=L, threads=threads, chunk=1, block_b=8, lanes=8, recip_mode=0, extract=0,
+                       strict_mode=1, distance_weight=1, clip=1, numa_domains=1,
+                       clip_cache=cache.encode())
+    walls, st = [], RefReconStats()
+    for i in range(warmup + steps):
+        vol = ctypes.c_void_p()
+        t0 = time.perf_counter()
+        rc = R.bp_reconstruct(h, ctypes.byref(p), ctypes.byref(vol), ctypes.byref(st))
+        dt = time.perf_counter() - t0
+        if rc != 0:
+            raise RuntimeError(R.bp_last_error().decode())
+        R.bp_volume_free(vol)
+        if i >= warmup:
+            walls.append(dt)
+    R.bp_stack_free(h)
+    return walls, st, int(cnt.value)
 
 
 def run_reference_arm(args):
     rank, world, local = dist_env()
     if rank != 0:
         return 0
-    import paper_1104_5243_b200 as bp  # datagen only (identical inputs to our arm)
-    stack, gen_s = make_stack(args)
-    px, mats = stack.pixels, stack.matrices
-    threads = os.cpu_count() or 1
     L = args.l
-    sample = args.cpu_views
-    for _ in range(args.warmup):
-        cpu_reference_run(px, mats, L, max(1, sample // 4), threads)
-    vals, walls = [], []
-    for _ in range(args.steps):
-        r = cpu_reference_run(px, mats, L, sample, threads)
-        vals.append(r["value"])
-        walls.append(r["wall_s"])
-    v = float(np.median(vals))
-    ms_per_step = float(np.median(walls)) * 1e3 * (args.views / sample)
+    threads = os.cpu_count() or 1
+    # bounded: one full reconstruction writes the reference's clip cache (untimed), then
+    # at most --ref-steps complete 496-view reconstructions are timed (about a minute each
+    # on 16 cores), whatever --steps asks for, so the arm ends within a few minutes
+    steps = max(1, min(args.steps, args.ref_steps))
+    warmup = 1 if args.warmup > 0 else 0
+    t0 = time.time()
+    sample = args.ref_sample_views or args.views
+    path = stack_file(args.views, args.seed, sample)
+    prep_s = time.time() - t0
+    walls, st, n = reference_reconstructions(path, L, steps, warmup, threads)
+    wall = float(np.median(walls))
+    nominal = n * L ** 3
+    v = nominal / wall / 1e9
     line = {
-        "metric": METRIC, "value": v, "unit": "GUP/s", "n_gpus": args.gpus, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
-        "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "impl": "reference",
-        "config": {"workload": f"{L}^3 x {args.views} views of 1248x960, config 3", "l": L,
-                   "views": args.views, "sample_views": sample},
-        "cpu_baseline": {"value": v, "unit": "GUP/s", "cores": threads, "kind": r["kind"],
-                         "sample": f"{sample} of {args.views} views, full {L}^3 volume; "
-                                   "ms_per_step extrapolated to all views"},
+        "metric": METRIC, "value": v, "unit": "GUP/s", "n_gpus": args.gpus, "steps": steps,
+        "steps_requested": args.steps, "warmup": warmup, "ms_per_step": wall * 1e3,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic", "impl": "reference",
+        "config": {"workload": f"{L}^3 x {n} views of 1248x960" + (
+                       f" (BASELINE config {CONFIG_OF_L[L]})" if L in CONFIG_OF_L and n == 496 else ""),
+                   "l": L, "views": n, "api": "reference bp_stack_read + bp_reconstruct (oracle/_ref, "
+                                      "unmodified reference sources)",
+                   "params": "threads=all lanes=8 block_b=8 clip=1 (reference clip_cache) "
+                             "recip=exact distance_weight=1"},
+        "cpu_baseline": {"value": v, "unit": "GUP/s", "cores": threads, "kind": "reference",
+                         "cpu_model": cpu_model(),
+                         "sample": (f"all {n} views" if n == args.views else
+                                    f"the first {n} of {args.views} views") +
+                                   f", full {L}^3 volume, {steps} timed bp_reconstruct call(s) after "
+                                   f"{warmup} untimed one (median wall time per call)"},
         "e2e": {"value": v, "unit": "GUP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "reference_stats": {"timed_region_s": st.seconds, "voxel_updates": int(st.voxel_updates),
+                            "gups_performed": st.gups, "clip_reduction": st.clip_reduction,
+                            "walls_s": walls},
+        "stack_prep_s": prep_s,
     }
     print(json.dumps(line), flush=True)
     return 0
+
+
+def cpu_baseline_subprocess(args, sample):
+    """The reference arm's code on the first `sample` views, in a child process (so this
+    process's GPU library stays out of the reference's way)."""
+    stack_file(args.views, args.seed, sample)
+    cmd = [sys.executable, os.path.abspath(__file__), "--impl", "reference", "--steps", "1",
+           "--warmup", "1", "--views", str(args.views), "--seed", str(args.seed), "--l", str(args.l),
+           "--ref-sample-views", str(sample)]
+    env = dict(os.environ)
+    for k in ("RANK", "WORLD_SIZE", "LOCAL_RANK"):
+        env.pop(k, None)
+    p = subprocess.run(cmd, capture_output=True, text=True, env=env)
+    if p.returncode != 0:
+        return None
+    return json.loads(p.stdout.strip().splitlines()[-1])
 
 
 # ---------------------------------------------------------------------------
@@ -444,14 +549,17 @@ def run_ours(args):
                "note": "e2e with GPU FDK preprocessing (cosine weight + Ram-Lak FFT filter, "
                        "bp_filter.cu) of each uploaded view; the reference has no filter"}
 
-    # ---- CPU baseline (rank 0, N=1 only) ----------------------------------------
+    # ---- CPU baseline (rank 0, N=1 only): the reference arm's code on a bounded sample
+    # (the first --cpu-views views, full volume), in a child process ----------------------
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        threads = os.cpu_count() or 1
-        r = cpu_reference_run(px, mats, L, args.cpu_views, threads)
-        cpu = {"value": r["value"], "unit": "GUP/s", "cores": threads, "kind": r["kind"],
-               "sample": f"{args.cpu_views} of {n} views over the full {L}^3 volume "
-                         f"(bp::reconstruct lanes=8 block_b=8 clip=1; wall {r['wall_s']:.2f} s)"}
+        r = cpu_baseline_subprocess(args, args.cpu_views)
+        if r is not None:
+            cb = r["cpu_baseline"]
+            cpu = {"value": r["value"], "unit": "GUP/s", "cores": cb["cores"], "kind": cb["kind"],
+                   "cpu_model": cb.get("cpu_model"),
+                   "sample": cb["sample"] + " (bp::reconstruct lanes=8 block_b=8 clip=1, "
+                             "reference clip_cache)"}
 
     if dist:
         vt = torch.tensor([visible], dtype=torch.float64, device=ctrl)
@@ -552,7 +660,16 @@ def main():
     ap.add_argument("--e2e-batch", type=int, default=32, help="views per launch, streamed e2e run")
     ap.add_argument("--seed", type=int, default=20110428)
     ap.add_argument("--strict", action="store_true", help="bitwise reference arithmetic")
-    ap.add_argument("--cpu-views", type=int, default=8)
+    ap.add_argument("--cpu-views", type=int, default=64,
+                    help="views of the bounded CPU-baseline sample in our arm (about 10-20 s)")
+    ap.add_argument("--ref-steps", type=int, default=2,
+                    help="reference arm: at most this many timed full reconstructions")
+    ap.add_argument("--ref-sample-views", type=int, default=0,
+                    help="reference arm: time the first N views only (0: all)")
+    ap.add_argument("--write-stack", default=None,
+                    help="write the seeded BASELINE stack (first --sample-views views) to this "
+                         "BPST path and exit")
+    ap.add_argument("--sample-views", type=int, default=0)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-fdk", action="store_true", help="skip the e2e run with GPU filtering")
     ap.add_argument("--no-pipelined", action="store_true",
@@ -561,6 +678,8 @@ def main():
                     help="N>1: compare rank 0's gathered volume with a single-context run")
     args = ap.parse_args()
     args.fast_off = args.strict
+    if args.write_stack:
+        return write_stack(args)
     if args.impl == "reference":
         return run_reference_arm(args)
     return run_ours(args)

@@ -173,14 +173,21 @@ static void* recon_worker(void* arg) {
     for (int k = 0; k < j->nviews; ++k) bpo_narrow(j->mats + 12 * k, Af + 12 * k);
     const size_t img_px = (size_t)j->isx * j->isy;
     /* z-slices round-robin over threads (partition_slices with chunk 1,
-     * scheduler.cpp:12-22); per voxel, views are applied in ascending order. */
-    for (int z = j->z0 + j->tid; z < j->z1; z += j->nthreads) {
-        for (int y = 0; y < L; ++y) {
-            float* line = j->out + ((size_t)(z - j->z0) * L + y) * L;
-            for (int k = 0; k < j->nviews; ++k)
-                j->updates += bpo_line_update(line, j->pixels + img_px * k, j->isx, j->isy,
-                                              Af + 12 * k, j->g, y, z, 0, L - 1,
-                                              j->distance_weight);
+     * scheduler.cpp:12-22); per voxel, views are applied in ascending order.
+     * Views are taken in blocks of 8 around the thread's lines (the reference's
+     * projection blocking, scheduler.cpp:77-100), so a block's images stay
+     * cache-resident; per-line view order is unchanged, hence bitwise the same. */
+    const int VB = 8;
+    for (int k0 = 0; k0 < j->nviews; k0 += VB) {
+        const int k1 = k0 + VB < j->nviews ? k0 + VB : j->nviews;
+        for (int z = j->z0 + j->tid; z < j->z1; z += j->nthreads) {
+            for (int y = 0; y < L; ++y) {
+                float* line = j->out + ((size_t)(z - j->z0) * L + y) * L;
+                for (int k = k0; k < k1; ++k)
+                    j->updates += bpo_line_update(line, j->pixels + img_px * k, j->isx, j->isy,
+                                                  Af + 12 * k, j->g, y, z, 0, L - 1,
+                                                  j->distance_weight);
+            }
         }
     }
     free(Af);

@@ -111,6 +111,7 @@ EXPORTED = [
     "bp_partition_slabs", "bp_slab_row_window", "bp_recon_ex_init", "bp_reconstruct_ex",
     "bp_selftest_rcp", "bp_build_info", "bp_gpu_read_lines", "bp_device_compare",
     "bp_gpu_clip_table", "bp_gpu_filter_views", "bp_ipc_handle", "bp_ipc_open", "bp_ipc_close",
+    "bp_gpu_release_cache",
 ]
 
 
@@ -474,6 +475,11 @@ def ipc_close(device_ptr: int) -> None:
     _check(lib().bp_ipc_close(C.c_void_p(base)))
 
 
+def release_cache() -> None:
+    """Frees the idle loaded contexts bp_reconstruct keeps between calls."""
+    _check(lib().bp_gpu_release_cache())
+
+
 def set_devices(devs) -> None:
     arr = (C.c_int * len(devs))(*devs)
     _check(lib().bp_gpu_set_devices(arr, len(devs)))
@@ -524,13 +530,21 @@ class GpuContext:
         self._h = h
 
     def backproject(self, image, matrix, copy=True) -> None:
-        img = np.ascontiguousarray(image, np.float32)
         m = np.ascontiguousarray(matrix, np.float64).reshape(12)
         if copy:
+            img = np.ascontiguousarray(image, np.float32)
             _check(lib().bp_gpu_backproject(self._h, _f(img), _d(m)))
         else:
-            # caller keeps `image` alive until finish()
-            _check(lib().bp_gpu_backproject_async(self._h, _f(img), _d(m)))
+            # zero-copy: the library reads `image` until finish(), so it must be the
+            # caller's own float32 C-contiguous buffer (a converted temporary would be
+            # freed on return while the upload is still pending)
+            if not (isinstance(image, np.ndarray) and image.dtype == np.float32
+                    and image.flags.c_contiguous):
+                raise ValueError("backproject(copy=False) needs a float32 C-contiguous array "
+                                 "that stays alive until finish()")
+            if image.size != self.isx * self.isy:
+                raise ValueError(f"image has {image.size} pixels, expected {self.isx * self.isy}")
+            _check(lib().bp_gpu_backproject_async(self._h, _f(image), _d(m)))
 
     def backproject_stack(self, stack: Stack) -> None:
         px, mats = stack.pixels, stack.matrices
@@ -543,6 +557,11 @@ class GpuContext:
             nz = self.z_end - self.z_begin
             if out is None:
                 out = np.empty((nz, self.l, self.l), np.float32)
+            elif not (isinstance(out, np.ndarray) and out.dtype == np.float32
+                      and out.flags.c_contiguous and out.flags.writeable
+                      and out.size >= nz * self.l * self.l):
+                raise ValueError(f"finish(out=...) needs a writeable float32 C-contiguous array "
+                                 f"of at least {nz * self.l * self.l} elements")
             _check(lib().bp_gpu_finish(self._h, _f(out), C.byref(st)))
         else:
             _check(lib().bp_gpu_finish(self._h, None, C.byref(st)))

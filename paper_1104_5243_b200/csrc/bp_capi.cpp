@@ -10,8 +10,10 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <fstream>
+#include <list>
 #include <map>
 #include <memory>
 #include <mutex>
@@ -57,13 +59,27 @@ int guarded(Fn&& fn) {
 using CtxKey = std::tuple<int, uint32_t, uint32_t, uint32_t, double, double, double, int, int, int,
                           int, int, int, int, int, int, int, double, double, double>;
 
+// Idle contexts, most recently released first.  Bounded by entry count and by the
+// device memory they hold (BP_CTX_CACHE_MB, default 16 GiB), least recently used
+// evicted first; an allocation failure in acquire() drains the cache and retries
+// once; bp_gpu_release_cache() drains it on request.
 struct CtxCache {
     std::mutex mu;
-    std::map<CtxKey, std::vector<std::unique_ptr<bpr::SlabContext>>> idle;
+    std::list<std::pair<CtxKey, std::unique_ptr<bpr::SlabContext>>> idle;
+    size_t bytes = 0;
 };
 CtxCache& cache() {
     static CtxCache* c = new CtxCache();
     return *c;
+}
+constexpr size_t kCacheEntries = 8;
+size_t cache_cap_bytes() {
+    static const size_t cap = [] {
+        size_t mb = (size_t)16 << 10;
+        if (const char* e = std::getenv("BP_CTX_CACHE_MB")) mb = (size_t)std::max(0L, std::atol(e));
+        return mb << 20;
+    }();
+    return cap;
 }
 
 CtxKey key_of(const bp_gpu_config& c) {
@@ -73,25 +89,62 @@ CtxKey key_of(const bp_gpu_config& c) {
                   c.recip_mode,    c.filter,      c.sid_mm,      c.sdd_mm,     c.pitch_mm};
 }
 
+// Removes every idle context (of `device`, or all when device < 0); the contexts are
+// destroyed after the lock is dropped.
+void drain_cache(int device) {
+    std::vector<std::unique_ptr<bpr::SlabContext>> dead;
+    {
+        auto& C = cache();
+        std::lock_guard<std::mutex> g(C.mu);
+        for (auto it = C.idle.begin(); it != C.idle.end();) {
+            if (device < 0 || it->second->device() == device) {
+                C.bytes -= it->second->device_bytes();
+                dead.push_back(std::move(it->second));
+                it = C.idle.erase(it);
+            } else {
+                ++it;
+            }
+        }
+    }
+}
+
 std::unique_ptr<bpr::SlabContext> acquire(const bp_gpu_config& c) {
     {
         auto& C = cache();
         std::lock_guard<std::mutex> g(C.mu);
-        auto it = C.idle.find(key_of(c));
-        if (it != C.idle.end() && !it->second.empty()) {
-            auto p = std::move(it->second.back());
-            it->second.pop_back();
-            return p;
-        }
+        const CtxKey k = key_of(c);
+        for (auto it = C.idle.begin(); it != C.idle.end(); ++it)
+            if (it->first == k) {
+                auto p = std::move(it->second);
+                C.bytes -= p->device_bytes();
+                C.idle.erase(it);
+                return p;
+            }
     }
-    return std::make_unique<bpr::SlabContext>(c);
+    try {
+        return std::make_unique<bpr::SlabContext>(c);
+    } catch (const bph::device_error&) {
+        // possibly out of device memory because of idle contexts: drop them, retry once
+        drain_cache(-1);
+        return std::make_unique<bpr::SlabContext>(c);
+    }
 }
 
 void release(std::unique_ptr<bpr::SlabContext> p) {
-    auto& C = cache();
-    std::lock_guard<std::mutex> g(C.mu);
-    auto& v = C.idle[key_of(p->config())];
-    if (v.size() < 2) v.push_back(std::move(p));
+    std::vector<std::unique_ptr<bpr::SlabContext>> dead;
+    {
+        auto& C = cache();
+        std::lock_guard<std::mutex> g(C.mu);
+        const size_t b = p->device_bytes();
+        if (b > cache_cap_bytes()) return;  // too large to keep idle (destroyed on return)
+        C.bytes += b;
+        C.idle.emplace_front(key_of(p->config()), std::move(p));
+        while (C.idle.size() > kCacheEntries || C.bytes > cache_cap_bytes()) {
+            C.bytes -= C.idle.back().second->device_bytes();
+            dead.push_back(std::move(C.idle.back().second));
+            C.idle.pop_back();
+        }
+    }
 }
 
 std::mutex g_dev_mu;
@@ -326,6 +379,10 @@ int bp_gpu_finish(bp_gpu_ctx* ctx, float* host_volume, bp_gpu_stats* stats) {
 int bp_gpu_unload(bp_gpu_ctx* ctx) {
     if (!ctx) return fail(BP_EINVAL, "null argument");
     return guarded([&] { delete ctx; });
+}
+
+int bp_gpu_release_cache(void) {
+    return guarded([&] { drain_cache(-1); });
 }
 
 int bp_gpu_volume_device(bp_gpu_ctx* ctx, float** dptr, int* z_begin, int* z_end) {

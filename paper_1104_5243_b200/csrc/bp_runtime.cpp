@@ -209,6 +209,24 @@ void SlabContext::mark_t0() {
 void SlabContext::bind() const { check(cudaSetDevice(dev_), "cudaSetDevice"); }
 
 SlabContext::SlabContext(const bp_gpu_config& cfg) : cfg_(cfg) {
+    // a failed allocation part-way through must not leak what was already allocated
+    try {
+        init();
+    } catch (...) {
+        release_all();
+        throw;
+    }
+}
+
+size_t SlabContext::device_bytes() const {
+    size_t b = (size_t)slots_ * isy_ * pitch_ * sizeof(float) + 3 * (size_t)(L_ + 160) * sizeof(float);
+    if (own_vol_) b += (size_t)nz_ * L_ * L_ * sizeof(float);
+    if (d_ringx_) b += (size_t)slots_ * (isy_ + 1) * pitch_ * sizeof(float2);
+    return b;
+}
+
+void SlabContext::init() {
+    const bp_gpu_config& cfg = cfg_;
     if (cfg.l < 1) throw bph::config_error("grid edge must be >= 1 voxel");
     if (cfg.isx < 2 || cfg.isy < 2) throw bph::config_error("detector must be at least 2x2 pixels");
     if (cfg.recip_mode < BP_RECIP_EXACT || cfg.recip_mode > BP_RECIP_HW_APPROX)
@@ -306,20 +324,22 @@ SlabContext::SlabContext(const bp_gpu_config& cfg) : cfg_(cfg) {
     reset_recon();
 }
 
-SlabContext::~SlabContext() {
+SlabContext::~SlabContext() { release_all(); }
+
+void SlabContext::release_all() noexcept {
     cudaSetDevice(dev_);
     if (s_comp_) cudaStreamSynchronize(s_comp_);
     if (s_prep_) cudaStreamSynchronize(s_prep_);
     if (s_aux_) cudaStreamSynchronize(s_aux_);
     if (s_copy_) cudaStreamSynchronize(s_copy_);
     if (s_d2h_) cudaStreamSynchronize(s_d2h_);
-    for (auto e : ev_chunk_) cudaEventDestroy(e);
-    for (auto e : ev_ready_) cudaEventDestroy(e);
-    for (auto e : ev_free_) cudaEventDestroy(e);
-    for (auto e : ev_prep_) cudaEventDestroy(e);
+    for (auto e : ev_chunk_) if (e) cudaEventDestroy(e);
+    for (auto e : ev_ready_) if (e) cudaEventDestroy(e);
+    for (auto e : ev_free_) if (e) cudaEventDestroy(e);
+    for (auto e : ev_prep_) if (e) cudaEventDestroy(e);
     for (auto& p : launch_ev_) {
-        cudaEventDestroy(p.first);
-        cudaEventDestroy(p.second);
+        if (p.first) cudaEventDestroy(p.first);
+        if (p.second) cudaEventDestroy(p.second);
     }
     for (cudaEvent_t e : {ev_t0_, ev_t1_, ev_h0_, ev_h1_, ev_d0_, ev_d1_})
         if (e) cudaEventDestroy(e);
@@ -329,13 +349,22 @@ SlabContext::~SlabContext() {
     if (s_copy_) cudaStreamDestroy(s_copy_);
     if (s_d2h_) cudaStreamDestroy(s_d2h_);
     if (own_vol_ && d_vol_) cudaFree(d_vol_);
-    cudaFree(d_ring_);
-    if (d_ringx_) cudaFree(d_ringx_);
-    cudaFree(d_wx_);
-    cudaFree(d_wy_);
-    cudaFree(d_wz_);
-    cudaFree(d_cnt_);
+    for (void* p : {(void*)d_ring_, (void*)d_ringx_, (void*)d_wx_, (void*)d_wy_, (void*)d_wz_,
+                    (void*)d_cnt_})
+        if (p) cudaFree(p);
     if (h_stage_) bph::pinned_free(h_stage_);
+    s_comp_ = s_prep_ = s_aux_ = s_copy_ = s_d2h_ = nullptr;
+    d_vol_ = d_ring_ = nullptr;
+    d_ringx_ = nullptr;
+    d_wx_ = d_wy_ = d_wz_ = nullptr;
+    d_cnt_ = nullptr;
+    h_stage_ = nullptr;
+    ev_chunk_.clear();
+    ev_ready_.clear();
+    ev_free_.clear();
+    ev_prep_.clear();
+    launch_ev_.clear();
+    ev_t0_ = ev_t1_ = ev_h0_ = ev_h1_ = ev_d0_ = ev_d1_ = nullptr;
     cudaGetLastError();
 }
 

@@ -74,9 +74,13 @@ public:
     int z_end() const { return z1_; }
     int device() const { return dev_; }
     const bp_gpu_config& config() const { return cfg_; }
+    // device memory this context holds (volume if owned, rings, tables)
+    size_t device_bytes() const;
     void bind() const;
 
 private:
+    void init();
+    void release_all() noexcept;  // frees whatever has been allocated (destructor, failed init)
     struct Pending {
         bpg::BatchArgs b;
         int rg;          // ring group holding the batch's projections
