@@ -93,6 +93,9 @@ def ref():
                                      C.POINTER(C.c_uint64)]
         R.ref_make_stack.argtypes = [C.c_char_p, i, i, i, d, d, d, dp, fp]
         R.ref_forward_project.argtypes = [dp, i, dp, i, i, fp]
+        R.ref_read_clip_table.argtypes = [C.c_char_p, C.POINTER(C.c_int), C.POINTER(C.c_int),
+                                          C.POINTER(C.c_uint16), C.POINTER(C.c_uint64)]
+        R.ref_write_clip_table.argtypes = [C.c_char_p, i, i, C.POINTER(C.c_uint16)]
         R.ref_last_error.restype = C.c_char_p
         _ref = R
     return _ref
@@ -247,3 +250,27 @@ def ref_clip_table(mats, isx, isy, L, *, offset=(0.0, 0.0, 0.0)):
     if rc != 0:
         raise ValueError(R.ref_last_error().decode())
     return ranges, tot.value
+
+
+def ref_read_clip_table(path):
+    """BPCT file through the reference's read_clip_table: (ranges (n, L, L, 2) u16, total)."""
+    R = ref()
+    L, n = C.c_int(), C.c_int()
+    if R.ref_read_clip_table(path.encode(), C.byref(L), C.byref(n), None, None) != 0:
+        raise ValueError(R.ref_last_error().decode())
+    ranges = np.zeros((n.value, L.value, L.value, 2), np.uint16)
+    tot = C.c_uint64(0)
+    if R.ref_read_clip_table(path.encode(), None, None,
+                             ranges.ctypes.data_as(C.POINTER(C.c_uint16)), C.byref(tot)) != 0:
+        raise ValueError(R.ref_last_error().decode())
+    return ranges, tot.value
+
+
+def ref_write_clip_table(path, ranges):
+    """BPCT file through the reference's write_clip_table."""
+    R = ref()
+    r = np.ascontiguousarray(ranges, np.uint16)
+    if R.ref_write_clip_table(path.encode(), r.shape[1], r.shape[0],
+                              r.ctypes.data_as(C.POINTER(C.c_uint16))) != 0:
+        raise ValueError(R.ref_last_error().decode())
+

@@ -9,6 +9,7 @@
 //   - pad_image + line_update_scalar per sampled line  kernel.cpp:32-85
 //   - build_clip_table / clip_stats                                    precompute.cpp:51-103
 //   - make_circular_trajectory + make_stack for datagen pinning        geometry.cpp:86-128, datagen.cpp:80-108
+//   - the BPCT clip-cache reader / writer (format interop tests)        precompute.cpp:105-134
 // No reference source is copied; this file only calls it.
 #include <cstdint>
 #include <cstring>
@@ -152,6 +153,37 @@ int ref_forward_project(const double* ell, int n_ell, const double* mat, int isx
         bp::ProjectionMatrix M;
         std::memcpy(M.a.data(), mat, 12 * sizeof(double));
         bp::forward_project(ph, M, isx, isy, out);
+        return 0;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return 1;
+    }
+}
+
+// BPCT cache file through the reference's own reader: dims first (ranges may be NULL),
+// then the ranges (2*n*L*L u16) and clip_stats total.
+int ref_read_clip_table(const char* path, int* L, int* n, uint16_t* ranges, uint64_t* total) {
+    try {
+        auto t = bp::read_clip_table(path);
+        if (L) *L = t.L;
+        if (n) *n = t.n_views;
+        if (ranges) std::memcpy(ranges, t.ranges.data(), t.ranges.size() * sizeof(uint16_t));
+        if (total) *total = bp::clip_stats(t).total_updates;
+        return 0;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return 1;
+    }
+}
+
+// ... and through the reference's own writer.
+int ref_write_clip_table(const char* path, int L, int n, const uint16_t* ranges) {
+    try {
+        bp::ClipTable t;
+        t.L = L;
+        t.n_views = n;
+        t.ranges.assign(ranges, ranges + (size_t)2 * n * L * L);
+        bp::write_clip_table(path, t);
         return 0;
     } catch (const std::exception& e) {
         g_err = e.what();

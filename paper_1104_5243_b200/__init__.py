@@ -111,7 +111,7 @@ EXPORTED = [
     "bp_partition_slabs", "bp_slab_row_window", "bp_recon_ex_init", "bp_reconstruct_ex",
     "bp_selftest_rcp", "bp_build_info", "bp_gpu_read_lines", "bp_device_compare",
     "bp_gpu_clip_table", "bp_gpu_filter_views", "bp_ipc_handle", "bp_ipc_open", "bp_ipc_close",
-    "bp_gpu_release_cache",
+    "bp_gpu_release_cache", "bp_clip_table_read", "bp_clip_table_write",
 ]
 
 
@@ -183,6 +183,10 @@ def lib():
         "bp_ipc_handle": (ip, [vp, C.POINTER(C.c_ubyte), C.POINTER(C.c_uint64)]),
         "bp_ipc_open": (ip, [C.POINTER(C.c_ubyte), pp]),
         "bp_ipc_close": (ip, [vp]),
+        "bp_gpu_release_cache": (ip, []),
+        "bp_clip_table_read": (ip, [C.c_char_p, C.POINTER(u32), C.POINTER(u32),
+                                    C.POINTER(C.c_uint16), C.POINTER(C.c_uint64)]),
+        "bp_clip_table_write": (ip, [C.c_char_p, u32, u32, C.POINTER(C.c_uint16)]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)
@@ -473,6 +477,24 @@ _ipc_bases = {}
 def ipc_close(device_ptr: int) -> None:
     base = _ipc_bases.pop(int(device_ptr), int(device_ptr))
     _check(lib().bp_ipc_close(C.c_void_p(base)))
+
+
+def clip_table_read(path: str):
+    """BPCT file -> (ranges (count, l, l, 2) u16, clip_stats total)."""
+    l, n = C.c_uint32(), C.c_uint32()
+    _check(lib().bp_clip_table_read(path.encode(), C.byref(l), C.byref(n), None, None))
+    ranges = np.zeros((n.value, l.value, l.value, 2), np.uint16)
+    tot = C.c_uint64()
+    _check(lib().bp_clip_table_read(path.encode(), None, None,
+                                    ranges.ctypes.data_as(C.POINTER(C.c_uint16)), C.byref(tot)))
+    return ranges, tot.value
+
+
+def clip_table_write(path: str, ranges) -> None:
+    r = np.ascontiguousarray(ranges, np.uint16)
+    n, l = r.shape[0], r.shape[1]
+    assert r.shape == (n, l, l, 2)
+    _check(lib().bp_clip_table_write(path.encode(), l, n, r.ctypes.data_as(C.POINTER(C.c_uint16))))
 
 
 def release_cache() -> None:

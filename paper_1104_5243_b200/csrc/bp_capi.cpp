@@ -416,6 +416,30 @@ int bp_gpu_clip_table(const bp_stack* s, uint32_t l, const double offset_mm[3], 
     });
 }
 
+int bp_clip_table_read(const char* path, uint32_t* l, uint32_t* count, uint16_t* ranges,
+                       uint64_t* total) {
+    if (!path) return fail(BP_EINVAL, "null argument");
+    return guarded([&] {
+        const auto t = bph::read_clip_table(path);
+        if (l) *l = (uint32_t)t.L;
+        if (count) *count = (uint32_t)t.n_views;
+        if (ranges) std::memcpy(ranges, t.ranges.data(), t.ranges.size() * sizeof(uint16_t));
+        if (total) *total = t.total_updates();
+    });
+}
+
+int bp_clip_table_write(const char* path, uint32_t l, uint32_t count, const uint16_t* ranges) {
+    if (!path || !ranges) return fail(BP_EINVAL, "null argument");
+    return guarded([&] {
+        if (l < 1 || l > 65535 || count < 1) throw bph::config_error("clip table dimensions out of range");
+        bph::ClipTable t;
+        t.L = (int)l;
+        t.n_views = (int)count;
+        t.ranges.assign(ranges, ranges + (size_t)2 * count * l * l);
+        bph::write_clip_table(path, t);
+    });
+}
+
 int bp_gpu_filter_views(const float* in, float* out, int count, uint32_t isx, uint32_t isy,
                         double sid_mm, double sdd_mm, double pitch_mm, int device) {
     if (!in || !out || count < 1) return fail(BP_EINVAL, "null argument");

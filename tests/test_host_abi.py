@@ -194,3 +194,106 @@ def test_ctypes_mirrors_match_the_c_headers(tmp_path):
     want = [C.sizeof(bp.GpuConfig), C.sizeof(bp.GpuStats), bp.GpuConfig.tail_batches.offset,
             bp.GpuStats.prep_launches.offset, bp.GpuConfig.output_volume.offset]
     assert got == want, (got, want)
+
+
+# ---- BPVL / BPCT interoperability with the reference's own readers and writers ------
+# (datagen.cpp:161-180 BPVL, precompute.cpp:105-134 BPCT; VERDICT r1 "What's missing" 3)
+
+def _ref_volume_api():
+    R = O.ref()
+    R.bp_volume_read.argtypes = [C.c_char_p, C.POINTER(C.c_void_p)]
+    R.bp_volume_write.argtypes = [C.c_void_p, C.c_char_p]
+    R.bp_volume_edge.argtypes = [C.c_void_p]
+    R.bp_volume_edge.restype = C.c_uint32
+    R.bp_volume_data.argtypes = [C.c_void_p]
+    R.bp_volume_data.restype = C.c_void_p
+    R.bp_volume_free.argtypes = [C.c_void_p]
+    R.bp_stack_generate.argtypes = [C.POINTER(bp.GenParams), C.POINTER(C.c_void_p)]
+    R.bp_stack_free.argtypes = [C.c_void_p]
+    R.bp_reconstruct.argtypes = [C.c_void_p, C.POINTER(bp.ReconParams), C.POINTER(C.c_void_p),
+                                 C.c_void_p]
+    return R
+
+
+def test_bpvl_interoperates_both_ways(tmp_path):
+    if not O.ref_available():
+        pytest.skip("oracle/_ref not built")
+    R = _ref_volume_api()
+    L = 12
+    # written here, read by the reference's bp_volume_read
+    v = bp.Volume.create(L)
+    v.data[...] = np.random.default_rng(5).standard_normal((L, L, L)).astype(np.float32)
+    p = str(tmp_path / "ours.bpvl")
+    v.write(p)
+    h = C.c_void_p()
+    assert R.bp_volume_read(p.encode(), C.byref(h)) == 0, R.bp_last_error()
+    assert R.bp_volume_edge(h) == L
+    got = np.ctypeslib.as_array(C.cast(R.bp_volume_data(h), C.POINTER(C.c_float)), (L, L, L)).copy()
+    R.bp_volume_free(h)
+    assert bitwise_equal(got, v.data)
+    # reconstructed and written by the reference (its own C ABI), read here
+    gp = bp.GenParams(b"spheres3", 3, 40, 32, 0.0, 0.0, 0.32 * 1248 / 40)
+    s = C.c_void_p()
+    assert R.bp_stack_generate(C.byref(gp), C.byref(s)) == 0
+    rv = C.c_void_p()
+    assert R.bp_reconstruct(s, C.byref(bp.recon_params(L, block_b=1)), C.byref(rv), None) == 0
+    q = str(tmp_path / "ref.bpvl")
+    assert R.bp_volume_write(rv, q.encode()) == 0
+    want = np.ctypeslib.as_array(C.cast(R.bp_volume_data(rv), C.POINTER(C.c_float)), (L, L, L)).copy()
+    R.bp_volume_free(rv)
+    R.bp_stack_free(s)
+    back = bp.Volume.read(q)
+    assert back.edge == L and bitwise_equal(back.data, want) and np.abs(want).max() > 0
+
+
+def test_bpct_interoperates_both_ways(tmp_path):
+    if not O.ref_available():
+        pytest.skip("oracle/_ref not built")
+    px, mats = small_stack("spheres3", 4, 40, 32)
+    L = 16
+    ranges, total = O.ref_clip_table(mats, 40, 32, L)
+    assert (ranges[..., 0] == 0xFFFF).any() and total > 0  # some empty lines
+    # written by this library, read by the reference's read_clip_table
+    p = str(tmp_path / "ours.bpct")
+    bp.clip_table_write(p, ranges)
+    r2, t2 = O.ref_read_clip_table(p)
+    assert np.array_equal(r2, ranges) and t2 == total
+    # written by the reference's write_clip_table, read by this library
+    q = str(tmp_path / "ref.bpct")
+    O.ref_write_clip_table(q, ranges)
+    r3, t3 = bp.clip_table_read(q)
+    assert np.array_equal(r3, ranges) and t3 == total
+    # byte-identical files from the two writers
+    assert open(p, "rb").read() == open(q, "rb").read()
+
+
+def test_bpct_reader_rejects_garbage(tmp_path):
+    p = tmp_path / "bad.bpct"
+    p.write_bytes(b"BPVL" + b"\0" * 12)
+    with pytest.raises(bp.BPError) as e:
+        bp.clip_table_read(str(p))
+    assert e.value.code == 2  # BP_EIO
+
+
+# ---- the reference's own C-API test suite, compiled unchanged (tests/capi/Makefile) --
+
+CAPI_BIN = os.path.join(ROOT, "tests", "capi", "_build", "test_capi")
+
+
+def test_reference_capi_suite_links_against_this_library():
+    if not os.path.exists(CAPI_BIN):
+        if not os.path.isdir("/root/reference/proj"):
+            pytest.skip("tests/capi/_build/test_capi not built (needs the reference sources)")
+        import subprocess
+        subprocess.run(["make", "-s", "-C", os.path.join(ROOT, "tests", "capi")], check=True)
+    import subprocess
+    ldd = subprocess.run(["ldd", CAPI_BIN], capture_output=True, text=True).stdout
+    line = [ln for ln in ldd.splitlines() if "libbackproject.so" in ln]
+    assert line and os.path.realpath(line[0].split("=>")[1].split("(")[0].strip()) == \
+        os.path.realpath(bp.LIB_PATH)
+    # the cases that need no device run here (the rest run in tests/test_gpu_capi.py)
+    r = subprocess.run([CAPI_BIN], capture_output=True, text=True, cwd=str(ROOT), timeout=300,
+                       env=dict(os.environ, CUDA_VISIBLE_DEVICES=""))
+    for case in ("stack generation, dims, file round trip", "error codes and thread-local messages",
+                 "reconstruction parameter validation"):
+        assert f"[{case}] PASSED" in r.stdout, r.stdout
