@@ -486,6 +486,35 @@ def run_ours(args):
     e2e_ctx.close()
     e2e_val = nominal_step * args.steps / e2e_s / 1e9
 
+    # ---- e2e_copy: the module path a RabbitCT-style harness uses -- bp_gpu_backproject
+    # (copy semantics: the image is staged before the call returns, so the caller may
+    # reuse its buffer) from ordinary PAGEABLE per-view buffers into a PAGEABLE host
+    # volume ------------------------------------------------
+    e2e_copy = None
+    if world == 1 and not args.no_copy_path:
+        pg_px = np.array(px, copy=True)  # pageable (numpy heap), not the library's pinned pool
+        pg_vol = np.empty((L, L, L), np.float32)
+        pg_vol.fill(0.0)
+        cctx = bp.GpuContext(L, isx, isy, device=device, strict=args.strict, view_batch=args.e2e_batch)
+        for _ in range(max(1, min(2, args.warmup))):
+            for k in range(n):
+                cctx.backproject(pg_px[k], mats[k], copy=True)
+            cctx.finish(out=pg_vol)
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            for k in range(n):
+                cctx.backproject(pg_px[k], mats[k], copy=True)
+            cctx.finish(out=pg_vol)
+        copy_s = time.perf_counter() - t0
+        cctx.close()
+        e2e_copy = {"value": nominal_step * args.steps / copy_s / 1e9, "unit": "GUP/s",
+                    "ms_per_step": copy_s * 1e3 / args.steps,
+                    "h2d_bytes_per_step": h2d // args.steps, "d2h_bytes_per_step": d2h // args.steps,
+                    "note": "bp_gpu_backproject (copy semantics) per view from pageable buffers, "
+                            "bp_gpu_finish into a pageable volume; staging and readback copies "
+                            "on the library's host copy pool"}
+        del pg_px, pg_vol
+
     # ---- e2e, back-to-back reconstructions: two module contexts on two host threads, so
     # one volume's readback (D2H) overlaps the next volume's upload (H2D) -- PCIe is full
     # duplex (tools/pcie_duplex_probe.py).  Every reconstruction still uploads its whole
@@ -634,6 +663,8 @@ def run_ours(args):
     }
     if e2e_pipe:
         line["e2e_pipelined"] = e2e_pipe
+    if e2e_copy:
+        line["e2e_copy"] = e2e_copy
     if fdk:
         line["fdk_e2e"] = fdk
     if gather_check is not None:
@@ -672,6 +703,8 @@ def main():
     ap.add_argument("--sample-views", type=int, default=0)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-fdk", action="store_true", help="skip the e2e run with GPU filtering")
+    ap.add_argument("--no-copy-path", action="store_true",
+                    help="skip the pageable copy-semantics e2e run (e2e_copy)")
     ap.add_argument("--no-pipelined", action="store_true",
                     help="skip the back-to-back (two-context) e2e run")
     ap.add_argument("--verify-gather", action="store_true",

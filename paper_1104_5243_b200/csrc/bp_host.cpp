@@ -7,6 +7,7 @@
 #include <algorithm>
 #include <cmath>
 #include <complex>
+#include <condition_variable>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -43,6 +44,100 @@ bool cuda_usable(PoolState& P) {
 }
 constexpr size_t kPoolCacheLimit = (size_t)16 << 30;
 }  // namespace
+
+namespace {
+
+// Fork-join pool: workers sleep on a condition variable; a job is a byte range split in
+// equal parts, part 0 copied by the caller.
+class CopyPool {
+public:
+    CopyPool() {
+        const unsigned hc = std::max(1u, std::thread::hardware_concurrency());
+        nworkers_ = (int)std::min(7u, hc > 2 ? hc / 2 - 1 : 0u);
+        for (int i = 0; i < nworkers_; ++i) th_.emplace_back([this, i] { run(i + 1); });
+    }
+    ~CopyPool() {
+        {
+            std::lock_guard<std::mutex> g(mu_);
+            stop_ = true;
+            ++gen_;
+        }
+        cv_.notify_all();
+        for (auto& t : th_) t.join();
+    }
+    void copy(void* dst, const void* src, size_t bytes) {
+        if (nworkers_ == 0 || bytes < ((size_t)1 << 20)) {
+            std::memcpy(dst, src, bytes);
+            return;
+        }
+        std::lock_guard<std::mutex> one(job_mu_);  // one job at a time
+        {
+            std::lock_guard<std::mutex> g(mu_);
+            dst_ = static_cast<char*>(dst);
+            src_ = static_cast<const char*>(src);
+            bytes_ = bytes;
+            pending_ = nworkers_;
+            ++gen_;
+        }
+        cv_.notify_all();
+        part(0);
+        std::unique_lock<std::mutex> g(mu_);
+        done_cv_.wait(g, [&] { return pending_ == 0; });
+    }
+
+private:
+    void part(int i) {
+        const int parts = nworkers_ + 1;
+        // 4 KB-aligned split points
+        auto at = [&](int k) { return std::min(bytes_, ((bytes_ * (size_t)k / parts) + 4095) & ~(size_t)4095); };
+        const size_t a = i == 0 ? 0 : at(i), b = i == parts - 1 ? bytes_ : at(i + 1);
+        if (b > a) std::memcpy(dst_ + a, src_ + a, b - a);
+    }
+    void run(int i) {
+        uint64_t seen = 0;
+        for (;;) {
+            {
+                std::unique_lock<std::mutex> g(mu_);
+                cv_.wait(g, [&] { return gen_ != seen; });
+                seen = gen_;
+                if (stop_) return;
+            }
+            part(i);
+            {
+                std::lock_guard<std::mutex> g(mu_);
+                if (--pending_ == 0) done_cv_.notify_one();
+            }
+        }
+    }
+    int nworkers_ = 0;
+    std::vector<std::thread> th_;
+    std::mutex mu_, job_mu_;
+    std::condition_variable cv_, done_cv_;
+    uint64_t gen_ = 0;
+    bool stop_ = false;
+    int pending_ = 0;
+    char* dst_ = nullptr;
+    const char* src_ = nullptr;
+    size_t bytes_ = 0;
+};
+
+CopyPool& copy_pool() {
+    static CopyPool* p = new CopyPool();  // never destroyed: workers may outlive statics
+    return *p;
+}
+
+}  // namespace
+
+void parallel_memcpy(void* dst, const void* src, size_t bytes) { copy_pool().copy(dst, src, bytes); }
+
+bool is_pageable(const void* p) {
+    cudaPointerAttributes a{};
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return true;
+    }
+    return a.type == cudaMemoryTypeUnregistered;
+}
 
 void* pinned_alloc(size_t bytes) {
     auto& P = pool();
@@ -196,32 +291,48 @@ std::vector<int> partition_slabs(const std::vector<Mat>& mats, int isx, int isy,
     const int L = g.L;
     if (G < 1) throw config_error("slab count must be >= 1");
     if (G > L) throw config_error("more slabs than z-slices");
-    // coarse lattice
-    const int nsx = std::min(L, 48);
-    const int vstride = std::max<int>(1, (int)mats.size() / 64);
-    std::vector<double> work((size_t)L, 0.0);
-    const int zsamples = std::min(L, 256);
-    std::vector<double> zw((size_t)zsamples, 0.0);
-    std::vector<std::array<float, 12>> fm;
-    for (size_t k = 0; k < mats.size(); k += (size_t)vstride) fm.push_back(narrowed(mats[k]));
+    // Cost model = the tiled kernel's work, not visible voxels: per layer of voxel
+    // blocks (the block shapes of tile_shape_for, bp_kernels.cu), the number of
+    // (block, view) pairs that survive the producer's cull -- the block's 8 corners
+    // projected, footprint [floor(min) - 1, floor(max) + 2] against the detector --
+    // times the block's voxels, plus a per-pair overhead (the per-view header, line
+    // constants and barrier, ~6% of a block's voxel work) and a per-
+    // slice volume read-modify-write term.  Culled pairs cost the producer only.
+    // Views are strided (every 4th of 496); the counts are exact for those views.
+    const int BX = L >= 512 ? 32 : 16, BY = L >= 512 ? 32 : (L >= 256 ? 16 : 8),
+              BZ = L >= 256 ? 8 : 4;
+    const int nbx = (L + BX - 1) / BX, nby = (L + BY - 1) / BY, nbz = (L + BZ - 1) / BZ;
+    const int vstride = std::max<int>(1, (int)mats.size() / 128);
+    std::vector<std::array<double, 12>> fm;
+    for (size_t k = 0; k < mats.size(); k += (size_t)vstride) fm.push_back(mats[k]);
+    std::vector<double> layer((size_t)nbz, 0.0);
     auto worker = [&](int t, int T) {
-        for (int zi = t; zi < zsamples; zi += T) {
-            const int z = (int)((zi + 0.5) * L / zsamples);
-            const double wz = g.wz(z);
-            double cnt = 0;
+        for (int bz = t; bz < nbz; bz += T) {
+            const double wz[2] = {g.wz(bz * BZ), g.wz(bz * BZ + BZ - 1)};
+            double pairs = 0;
             for (const auto& A : fm)
-                for (int yi = 0; yi < nsx; ++yi) {
-                    const double wy = g.wy((int)((yi + 0.5) * L / nsx));
-                    for (int xi = 0; xi < nsx; ++xi) {
-                        const double wx = g.wx((int)((xi + 0.5) * L / nsx));
-                        const double w = A[2] * wx + A[5] * wy + A[8] * wz + A[11];
-                        if (!(w > 0)) continue;
-                        const double u = (A[0] * wx + A[3] * wy + A[6] * wz + A[9]) / w;
-                        const double v = (A[1] * wx + A[4] * wy + A[7] * wz + A[10]) / w;
-                        if (u >= -1.0 && u < isx && v >= -1.0 && v < isy) cnt += 1;
+                for (int by = 0; by < nby; ++by) {
+                    const double wy[2] = {g.wy(by * BY), g.wy(by * BY + BY - 1)};
+                    for (int bx = 0; bx < nbx; ++bx) {
+                        const double wx[2] = {g.wx(bx * BX), g.wx(bx * BX + BX - 1)};
+                        double umin = 1e30, umax = -1e30, vmin = 1e30, vmax = -1e30;
+                        bool sane = true;
+                        for (int c = 0; c < 8; ++c) {
+                            const double X = wx[c & 1], Y = wy[(c >> 1) & 1], Z = wz[c >> 2];
+                            const double w = A[2] * X + A[5] * Y + A[8] * Z + A[11];
+                            if (!(w > 0)) { sane = false; break; }
+                            const double u = (A[0] * X + A[3] * Y + A[6] * Z + A[9]) / w;
+                            const double v = (A[1] * X + A[4] * Y + A[7] * Z + A[10]) / w;
+                            umin = std::min(umin, u); umax = std::max(umax, u);
+                            vmin = std::min(vmin, v); vmax = std::max(vmax, v);
+                        }
+                        if (sane && (std::floor(umax) + 2 < 0 || std::floor(umin) - 1 > isx - 1 ||
+                                     std::floor(vmax) + 2 < 0 || std::floor(vmin) - 1 > isy - 1))
+                            continue;  // culled: no consumer work
+                        pairs += 1;
                     }
                 }
-            zw[(size_t)zi] = cnt + 1e-3;  // keep empty slices slightly positive
+            layer[(size_t)bz] = pairs;
         }
     };
     {
@@ -230,14 +341,16 @@ std::vector<int> partition_slabs(const std::vector<Mat>& mats, int isx, int isy,
         for (int t = 0; t < T; ++t) th.emplace_back(worker, t, T);
         for (auto& x : th) x.join();
     }
-    for (int z = 0; z < L; ++z) {
-        int zi = std::min(zsamples - 1, (int)((double)z * zsamples / L));
-        work[(size_t)z] = zw[(size_t)zi];
-    }
+    // per-slice cost in voxel-update units (per view)
+    const double per_pair = (double)BX * BY * 1.06;       // one slice of a block, + overhead
+    const double rmw = (double)nbx * BX * nby * BY * 0.02;  // volume read/write per slice
+    std::vector<double> work((size_t)L, 0.0);
+    for (int z = 0; z < L; ++z) work[(size_t)z] = layer[(size_t)(z / BZ)] * per_pair + rmw + 1e-3;
     std::vector<double> cum((size_t)L + 1, 0.0);
     for (int z = 0; z < L; ++z) cum[(size_t)z + 1] = cum[(size_t)z] + work[(size_t)z];
     const double total = cum[(size_t)L];
-    const int align = (L / G >= 32) ? 8 : 1;
+    // slab bounds on block-layer boundaries when the slabs are thick enough
+    const int align = (L / G >= 4 * BZ) ? BZ : 1;
     std::vector<int> b((size_t)G + 1, 0);
     b[0] = 0;
     b[(size_t)G] = L;

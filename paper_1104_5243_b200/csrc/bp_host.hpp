@@ -36,6 +36,14 @@ struct device_error : std::runtime_error {  // CUDA failures -> BP_EINTERNAL
 // build stacks / read files).
 void* pinned_alloc(size_t bytes);
 void pinned_free(void* p);
+
+// memcpy split over a persistent fork-join pool of host threads (the caller takes a
+// share): the copy-semantics staging of bp_gpu_backproject and the readback into a
+// pageable host volume.  One copy runs at a time (callers queue); small copies stay
+// on the calling thread.
+void parallel_memcpy(void* dst, const void* src, size_t bytes);
+// true when p is ordinary pageable host memory (not page-locked, not device memory)
+bool is_pageable(const void* p);
 bool pinned_is_device_pinned(const void* p);
 void pinned_trim();
 

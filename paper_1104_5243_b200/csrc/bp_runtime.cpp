@@ -307,6 +307,8 @@ void SlabContext::init() {
     check(cudaStreamCreateWithFlags(&s_d2h_, cudaStreamNonBlocking), "stream");
     ev_chunk_.resize((size_t)tail_chunks_);
     for (auto& e : ev_chunk_) check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+    ev_dchunk_.resize((size_t)tail_chunks_);
+    for (auto& e : ev_dchunk_) check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
     ev_ready_.resize((size_t)R_);
     ev_free_.resize((size_t)R_);
     ev_prep_.resize((size_t)R_);
@@ -334,6 +336,7 @@ void SlabContext::release_all() noexcept {
     if (s_copy_) cudaStreamSynchronize(s_copy_);
     if (s_d2h_) cudaStreamSynchronize(s_d2h_);
     for (auto e : ev_chunk_) if (e) cudaEventDestroy(e);
+    for (auto e : ev_dchunk_) if (e) cudaEventDestroy(e);
     for (auto e : ev_ready_) if (e) cudaEventDestroy(e);
     for (auto e : ev_free_) if (e) cudaEventDestroy(e);
     for (auto e : ev_prep_) if (e) cudaEventDestroy(e);
@@ -353,6 +356,8 @@ void SlabContext::release_all() noexcept {
                     (void*)d_cnt_})
         if (p) cudaFree(p);
     if (h_stage_) bph::pinned_free(h_stage_);
+    if (h_bounce_) bph::pinned_free(h_bounce_);
+    h_bounce_ = nullptr;
     s_comp_ = s_prep_ = s_aux_ = s_copy_ = s_d2h_ = nullptr;
     d_vol_ = d_ring_ = nullptr;
     d_ringx_ = nullptr;
@@ -360,6 +365,7 @@ void SlabContext::release_all() noexcept {
     d_cnt_ = nullptr;
     h_stage_ = nullptr;
     ev_chunk_.clear();
+    ev_dchunk_.clear();
     ev_ready_.clear();
     ev_free_.clear();
     ev_prep_.clear();
@@ -414,11 +420,17 @@ void SlabContext::backproject(const float* image, const double* A, bool copy) {
     if (r1 > r0) {
         const float* src = image + (size_t)r0 * isx_;
         if (copy) {
-            if (!h_stage_)
+            if (!h_stage_) {
                 h_stage_ = static_cast<float*>(
                     bph::pinned_alloc((size_t)slots_ * isy_ * isx_ * sizeof(float)));
+                // rows outside a view's window may ride along in a 2-D window run (never
+                // read by any kernel); keep them finite
+                std::memset(h_stage_, 0, (size_t)slots_ * isy_ * isx_ * sizeof(float));
+            }
             float* stg = h_stage_ + (size_t)slot * isy_ * isx_ + (size_t)r0 * isx_;
-            std::memcpy(stg, src, (size_t)(r1 - r0) * isx_ * sizeof(float));
+            // the caller may reuse `image` when this returns: copy now, on several host
+            // threads (a pageable source reads at a fraction of PCIe speed per thread)
+            bph::parallel_memcpy(stg, src, (size_t)(r1 - r0) * isx_ * sizeof(float));
             src = stg;
         }
         if (!any_h2d_) {
@@ -427,21 +439,38 @@ void SlabContext::backproject(const float* image, const double* A, bool copy) {
         }
         float* dst = d_ring_ + (size_t)slot * isy_ * pitch_ + (size_t)r0 * pitch_;
         if (pitch_ == isx_) {
-            // coalesce views that are contiguous both in host memory and in the ring
-            // (consecutive images of one stack into consecutive slots, full windows):
-            // PCIe H2D reaches ~55 GB/s with >=16 MB copies vs ~52.5 GB/s at 4.8 MB
-            // per view (tools/h2d_probe.py)
-            const size_t bytes = (size_t)(r1 - r0) * isx_ * sizeof(float);
-            const char* cs = reinterpret_cast<const char*>(src);
-            char* cd = reinterpret_cast<char*>(dst);
-            if (run_bytes_ > 0 && cs == run_src_ + run_bytes_ && cd == run_dst_ + run_bytes_ &&
-                run_bytes_ + bytes <= run_limit_) {
-                run_bytes_ += bytes;
-            } else {
+            // Views whose images are equally spaced in host memory (consecutive images of
+            // one stack, or consecutive staging slots) and land in consecutive ring slots
+            // form one copy: a plain copy when every window is the full detector, else ONE
+            // 2-D copy of the run's union row window (height = views).  A z-slab's per-view
+            // windows move with the view, so per-view ~1 MB copies reached only ~17 GB/s;
+            // the union costs a few % more rows.  (tools/h2d_probe.py: >= 16 MB copies
+            // run at ~55 GB/s.)
+            const size_t view_bytes = (size_t)isx_ * isy_ * sizeof(float);
+            const size_t win_bytes = (size_t)(r1 - r0) * isx_ * sizeof(float);
+            const char* img = reinterpret_cast<const char*>(src) - (size_t)r0 * isx_ * sizeof(float);
+            bool extend = run_n_ > 0 && img == run_img0_ + run_n_ * view_bytes &&
+                          slot == run_slot0_ + run_n_;
+            if (extend) {
+                const int u0 = std::min(r0, run_r0_), u1 = std::max(r1, run_r1_);
+                const size_t ubytes = (size_t)(u1 - u0) * isx_ * sizeof(float) * (run_n_ + 1);
+                extend = ubytes <= run_limit_ &&
+                         ubytes <= (size_t)(1.15 * (double)(run_actual_ + win_bytes)) + 4 * view_bytes / 16;
+                if (extend) {
+                    run_r0_ = u0;
+                    run_r1_ = u1;
+                    run_actual_ += win_bytes;
+                    ++run_n_;
+                }
+            }
+            if (!extend) {
                 issue_run();
-                run_src_ = cs;
-                run_dst_ = cd;
-                run_bytes_ = bytes;
+                run_img0_ = img;
+                run_slot0_ = slot;
+                run_n_ = 1;
+                run_r0_ = r0;
+                run_r1_ = r1;
+                run_actual_ = win_bytes;
             }
         } else
             check(cudaMemcpy2DAsync(dst, (size_t)pitch_ * sizeof(float), src,
@@ -666,9 +695,19 @@ void SlabContext::launch_pending_front(bool final_pass) {
 }
 
 void SlabContext::issue_run() {
-    if (run_bytes_ == 0) return;
-    check(cudaMemcpyAsync(run_dst_, run_src_, run_bytes_, cudaMemcpyHostToDevice, s_copy_), "H2D");
-    run_bytes_ = 0;
+    if (run_n_ == 0) return;
+    const size_t row = (size_t)isx_ * sizeof(float);
+    const size_t view_bytes = row * isy_;
+    char* dst = reinterpret_cast<char*>(d_ring_ + (size_t)run_slot0_ * isy_ * pitch_) + (size_t)run_r0_ * row;
+    const char* src = run_img0_ + (size_t)run_r0_ * row;
+    const size_t width = (size_t)(run_r1_ - run_r0_) * row;
+    if (width == view_bytes || run_n_ == 1)  // contiguous: full windows, or one view
+        check(cudaMemcpyAsync(dst, src, width + (size_t)(run_n_ - 1) * view_bytes,
+                              cudaMemcpyHostToDevice, s_copy_), "H2D");
+    else
+        check(cudaMemcpy2DAsync(dst, view_bytes, src, view_bytes, width, (size_t)run_n_,
+                                cudaMemcpyHostToDevice, s_copy_), "H2D (2-D window run)");
+    run_n_ = 0;
 }
 
 void SlabContext::flush() {
@@ -690,6 +729,19 @@ void SlabContext::finish(float* host_volume, bp_gpu_stats* st) {
     flush();
     const size_t vbytes = (size_t)nz_ * L_ * L_ * sizeof(float);
     bool d2h_done = false;
+    // a pageable destination is read back through a pinned bounce buffer, each z-chunk
+    // copied out by the host thread pool as soon as its D2H lands
+    float* const dest = host_volume;
+    const bool bounce = host_volume && bph::is_pageable(host_volume);
+    if (bounce) {
+        if (!h_bounce_ || bounce_bytes_ < vbytes) {
+            if (h_bounce_) bph::pinned_free(h_bounce_);
+            h_bounce_ = static_cast<float*>(bph::pinned_alloc(vbytes));
+            bounce_bytes_ = vbytes;
+        }
+        host_volume = h_bounce_;
+    }
+    std::vector<std::pair<size_t, size_t>> chunks;  // (offset, count) of the D2H copies
     if (host_volume && !pending_.empty() && tiled_ && tail_chunks_ > 1 && nz_ >= 2 * ts_.bz) {
         // chunk-major tail: for each z-chunk run all deferred batches (ascending
         // view order per voxel is preserved), then stream that chunk back while the
@@ -717,6 +769,8 @@ void SlabContext::finish(float* host_volume, bp_gpu_stats* st) {
             check(cudaMemcpyAsync(host_volume + off, result() + off, n * sizeof(float),
                                   cudaMemcpyDefault, s_d2h_),
                   "D2H");
+            check(cudaEventRecord(ev_dchunk_[(size_t)c], s_d2h_), "event");
+            chunks.emplace_back(off, n);
         }
         any_launch_ = true;
         for (const auto& p : pending_) {
@@ -740,7 +794,15 @@ void SlabContext::finish(float* host_volume, bp_gpu_stats* st) {
         check(cudaEventRecord(ev_d0_, s_comp_), "event");
         check(cudaMemcpyAsync(host_volume, result(), vbytes, cudaMemcpyDefault, s_comp_), "D2H");
         check(cudaEventRecord(ev_d1_, s_comp_), "event");
+        check(cudaEventRecord(ev_dchunk_[0], s_comp_), "event");
+        chunks.emplace_back(0, vbytes / sizeof(float));
     }
+    if (bounce)
+        for (size_t c = 0; c < chunks.size(); ++c) {
+            check(cudaEventSynchronize(ev_dchunk_[c]), "D2H chunk");
+            bph::parallel_memcpy(dest + chunks[c].first, h_bounce_ + chunks[c].first,
+                                 chunks[c].second * sizeof(float));
+        }
     unsigned long long cnt[8] = {0};
     check(cudaMemcpyAsync(cnt, d_cnt_, sizeof cnt, cudaMemcpyDeviceToHost, s_comp_), "counters");
     check(cudaMemsetAsync(d_cnt_, 0, sizeof cnt, s_comp_), "counters");

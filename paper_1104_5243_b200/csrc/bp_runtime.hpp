@@ -152,11 +152,16 @@ private:
     uint64_t batch_index_ = 0;
     cudaStream_t s_d2h_ = nullptr;
     std::vector<cudaEvent_t> ev_chunk_;
+    std::vector<cudaEvent_t> ev_dchunk_;  // a chunk's D2H has landed (pageable readback)
+    float* h_bounce_ = nullptr;           // pinned bounce for a pageable host volume
+    size_t bounce_bytes_ = 0;
 
-    // coalesced H2D run [run_src_, +run_bytes_) -> [run_dst_, ...) on s_copy_
-    const char* run_src_ = nullptr;
-    char* run_dst_ = nullptr;
-    size_t run_bytes_ = 0, run_limit_ = (size_t)32 << 20;
+    // pending H2D run on s_copy_: run_n_ views whose images start at run_img0_ + i * view
+    // bytes, into ring slots run_slot0_ + i, rows [run_r0_, run_r1_) (the union of their
+    // row windows); run_actual_ = the views' own window bytes
+    const char* run_img0_ = nullptr;
+    int run_slot0_ = 0, run_n_ = 0, run_r0_ = 0, run_r1_ = 0;
+    size_t run_actual_ = 0, run_limit_ = (size_t)32 << 20;
 
     // per-reconstruction state
     bpg::BatchArgs cur_{};

@@ -9,8 +9,11 @@ build (bp_partition_slabs); each slab is reconstructed on this GPU:
 A G-GPU run takes as long as its slowest slab (each GPU has its own PCIe link on an
 8 x B200 box), plus the fused slab gather (the final kernel stores into rank 0's volume
 over NVLink; not modelled). Efficiency = T1 / (G * max_g T_g).
-Usage: python tools/scaling_projection.py [L=1024]"""
-import sys, time
+Usage: python tools/scaling_projection.py [L=1024]
+Env: E2E_BATCH (views per launch of a z-slab's streamed run when G > 1; default 124: with
+row windows a slab uploads ~20-30% of each view, so a larger batch costs little fill time
+and saves volume read-modify-write passes), VERBOSE=1 (per-slab times)."""
+import os, sys, time
 sys.path.insert(0, ".")
 import paper_1104_5243_b200 as bp
 
@@ -19,6 +22,8 @@ s = bp.Stack.baseline(n_views=496, isx=1248, isy=960)
 px, mats = s.pixels, s.matrices
 n = 496
 B = 248 if L < 2048 else 124
+EB = int(os.environ.get("E2E_BATCH", "124"))
+verbose = os.environ.get("VERBOSE") == "1"
 res, e2e = {}, {}
 host = bp.Volume.create(L)  # one pinned host volume; each slab reads back into its part
 print(f"| G | slab bounds | slowest slab, resident ms | projected resident efficiency | slowest slab, e2e ms | projected e2e efficiency |")
@@ -34,7 +39,8 @@ for G in (1, 2, 4, 8):
             c.time_resident(1)
             tr.append(min(c.time_resident(1)[0] for _ in range(2)))
         out = host.data[z0:z1]
-        with bp.GpuContext(L, 1248, 960, device=0, z_begin=z0, z_end=z1, strict=False, view_batch=32) as c:
+        eb = 32 if G == 1 else EB
+        with bp.GpuContext(L, 1248, 960, device=0, z_begin=z0, z_end=z1, strict=False, view_batch=eb) as c:
             c.backproject_stack(s)
             c.finish(out=out)
             best = 1e30
@@ -44,6 +50,9 @@ for G in (1, 2, 4, 8):
                 c.finish(out=out)
                 best = min(best, (time.perf_counter() - t0) * 1e3)
             te.append(best)
+        if verbose:
+            print(f"  G={G} slab [{z0},{z1}): resident {tr[-1]:.1f} ms, e2e {te[-1]:.1f} ms (batch {eb})",
+                  flush=True)
     res[G], e2e[G] = max(tr), max(te)
     print(f"| {G} | {bounds} | {res[G]:.1f} | {res[1] / (G * res[G]):.3f} | {e2e[G]:.1f} | "
           f"{e2e[1] / (G * e2e[G]):.3f} |", flush=True)
