@@ -5,6 +5,11 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#if defined(__SSE2__)
+#include <emmintrin.h>
+#endif
+#include <atomic>
+#include <chrono>
 #include <cmath>
 #include <complex>
 #include <condition_variable>
@@ -47,20 +52,61 @@ constexpr size_t kPoolCacheLimit = (size_t)16 << 30;
 
 namespace {
 
-// Fork-join pool: workers sleep on a condition variable; a job is a byte range split in
-// equal parts, part 0 copied by the caller.
+// Copy with non-temporal (streaming) stores: the destination (pinned staging that a DMA
+// reads next, or the caller's volume) is not re-read by this thread, and streaming
+// stores skip the read-for-ownership of every destination line -- a third of the memory
+// traffic of a cached memcpy, which matters while a full-rate H2D reads the same DRAM.
+void stream_copy(char* dst, const char* src, size_t n) {
+#if defined(__SSE2__)
+    // head: up to 16-byte alignment of the destination
+    const size_t head = std::min(n, (size_t)((16 - ((uintptr_t)dst & 15)) & 15));
+    std::memcpy(dst, src, head);
+    dst += head;
+    src += head;
+    n -= head;
+    size_t i = 0;
+    for (; i + 64 <= n; i += 64) {
+        const __m128i a = _mm_loadu_si128(reinterpret_cast<const __m128i*>(src + i));
+        const __m128i b = _mm_loadu_si128(reinterpret_cast<const __m128i*>(src + i + 16));
+        const __m128i c = _mm_loadu_si128(reinterpret_cast<const __m128i*>(src + i + 32));
+        const __m128i d = _mm_loadu_si128(reinterpret_cast<const __m128i*>(src + i + 48));
+        _mm_stream_si128(reinterpret_cast<__m128i*>(dst + i), a);
+        _mm_stream_si128(reinterpret_cast<__m128i*>(dst + i + 16), b);
+        _mm_stream_si128(reinterpret_cast<__m128i*>(dst + i + 32), c);
+        _mm_stream_si128(reinterpret_cast<__m128i*>(dst + i + 48), d);
+    }
+    _mm_sfence();  // streaming stores are weakly ordered: drain before the job completes
+    std::memcpy(dst + i, src + i, n - i);
+#else
+    std::memcpy(dst, src, n);
+#endif
+}
+
+// Fork-join pool for the staging copies of copy-semantics uploads and the pageable
+// readback: a job is a byte range split in equal parts, part 0 copied by the caller.
+// Jobs arrive back to back (one ~4.8 MB view every ~80 us during a reconstruction), so
+// idle workers spin on the job counter for up to 2 ms before sleeping on a
+// condition variable, and the caller spins on the completion count: a condition-variable
+// wake-up per job (tens of us for 7 workers) held the per-view copy to ~22 GB/s on the
+// box, against ~60 GB/s for 8 memcpy threads running beside a full-rate H2D
+// (tools/host_memcpy_probe.cpp).
 class CopyPool {
 public:
     CopyPool() {
         const unsigned hc = std::max(1u, std::thread::hardware_concurrency());
-        nworkers_ = (int)std::min(7u, hc > 2 ? hc / 2 - 1 : 0u);
+        // 12 copy threads on the 16-core box: 8 -> 12 measured e2e_copy 68.0 -> 61.9 ms
+        // (14 and 16 no better; the H2D reading the staging shares the same DRAM)
+        nworkers_ = (int)std::min(11u, hc > 2 ? hc * 3 / 4 - 1 : 0u);
+        // A/B knobs: worker count, spin time before sleeping (0 = sleep at once)
+        if (const char* e = std::getenv("BP_COPY_THREADS")) nworkers_ = std::max(0, std::atoi(e) - 1);
+        if (const char* e = std::getenv("BP_COPY_SPIN_US")) spin_us_ = std::max(0, std::atoi(e));
         for (int i = 0; i < nworkers_; ++i) th_.emplace_back([this, i] { run(i + 1); });
     }
     ~CopyPool() {
         {
             std::lock_guard<std::mutex> g(mu_);
-            stop_ = true;
-            ++gen_;
+            stop_.store(true);
+            gen_.fetch_add(1, std::memory_order_release);
         }
         cv_.notify_all();
         for (auto& t : th_) t.join();
@@ -71,51 +117,55 @@ public:
             return;
         }
         std::lock_guard<std::mutex> one(job_mu_);  // one job at a time
+        dst_ = static_cast<char*>(dst);
+        src_ = static_cast<const char*>(src);
+        bytes_ = bytes;
+        pending_.store(nworkers_, std::memory_order_relaxed);
         {
+            // under mu_ so that a worker between its last spin check and cv wait sees it
             std::lock_guard<std::mutex> g(mu_);
-            dst_ = static_cast<char*>(dst);
-            src_ = static_cast<const char*>(src);
-            bytes_ = bytes;
-            pending_ = nworkers_;
-            ++gen_;
+            gen_.fetch_add(1, std::memory_order_release);
         }
         cv_.notify_all();
         part(0);
-        std::unique_lock<std::mutex> g(mu_);
-        done_cv_.wait(g, [&] { return pending_ == 0; });
+        while (pending_.load(std::memory_order_acquire) > 0) {
+        }
     }
 
 private:
+    int spin_us_ = 2000;
     void part(int i) {
         const int parts = nworkers_ + 1;
         // 4 KB-aligned split points
         auto at = [&](int k) { return std::min(bytes_, ((bytes_ * (size_t)k / parts) + 4095) & ~(size_t)4095); };
         const size_t a = i == 0 ? 0 : at(i), b = i == parts - 1 ? bytes_ : at(i + 1);
-        if (b > a) std::memcpy(dst_ + a, src_ + a, b - a);
+        if (b > a) stream_copy(dst_ + a, src_ + a, b - a);
     }
     void run(int i) {
         uint64_t seen = 0;
         for (;;) {
-            {
-                std::unique_lock<std::mutex> g(mu_);
-                cv_.wait(g, [&] { return gen_ != seen; });
-                seen = gen_;
-                if (stop_) return;
+            const auto t0 = std::chrono::steady_clock::now();
+            unsigned spins = 0;
+            while (gen_.load(std::memory_order_acquire) == seen) {
+                if ((++spins & 255u) == 0 &&
+                    std::chrono::steady_clock::now() - t0 > std::chrono::microseconds(spin_us_)) {
+                    std::unique_lock<std::mutex> g(mu_);
+                    cv_.wait(g, [&] { return gen_.load(std::memory_order_acquire) != seen; });
+                }
             }
+            seen = gen_.load(std::memory_order_acquire);
+            if (stop_.load()) return;
             part(i);
-            {
-                std::lock_guard<std::mutex> g(mu_);
-                if (--pending_ == 0) done_cv_.notify_one();
-            }
+            pending_.fetch_sub(1, std::memory_order_acq_rel);
         }
     }
     int nworkers_ = 0;
     std::vector<std::thread> th_;
     std::mutex mu_, job_mu_;
-    std::condition_variable cv_, done_cv_;
-    uint64_t gen_ = 0;
-    bool stop_ = false;
-    int pending_ = 0;
+    std::condition_variable cv_;
+    std::atomic<uint64_t> gen_{0};
+    std::atomic<bool> stop_{false};
+    std::atomic<int> pending_{0};
     char* dst_ = nullptr;
     const char* src_ = nullptr;
     size_t bytes_ = 0;

@@ -263,8 +263,11 @@ void SlabContext::init() {
     const int tail_default = (z1_ - z0_ < L_) ? 5 : 3;
     tail_batches_ = std::max(0, std::min(R_ - 2, cfg.tail_batches >= 0 ? cfg.tail_batches : tail_default));
     tail_chunks_ = 8;
+    // a pageable destination adds a host copy per chunk after its D2H; smaller chunks
+    // leave less of it exposed after the last one (e2e_copy 61.9 -> 60.9 ms at 512^3)
+    bounce_chunks_ = 16;
     if (const char* e = std::getenv("BP_TAIL_BATCHES")) tail_batches_ = std::max(0, std::atoi(e));
-    if (const char* e = std::getenv("BP_TAIL_CHUNKS")) tail_chunks_ = std::max(1, std::atoi(e));
+    if (const char* e = std::getenv("BP_TAIL_CHUNKS")) bounce_chunks_ = tail_chunks_ = std::max(1, std::atoi(e));
     if (const char* e = std::getenv("BP_H2D_RUN_MB")) run_limit_ = (size_t)std::max(0, std::atoi(e)) << 20;
     if (const char* e = std::getenv("BP_NO_PAIR")) pair_ok_ = std::atoi(e) == 0;
     out_vol_ = cfg.output_volume;
@@ -305,9 +308,9 @@ void SlabContext::init() {
     if (const char* e = std::getenv("BP_NO_OVERLAP_EXPAND")) overlap_expand_ = std::atoi(e) == 0;
     check(cudaStreamCreateWithFlags(&s_copy_, cudaStreamNonBlocking), "stream");
     check(cudaStreamCreateWithFlags(&s_d2h_, cudaStreamNonBlocking), "stream");
-    ev_chunk_.resize((size_t)tail_chunks_);
+    ev_chunk_.resize((size_t)std::max(tail_chunks_, bounce_chunks_));
     for (auto& e : ev_chunk_) check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
-    ev_dchunk_.resize((size_t)tail_chunks_);
+    ev_dchunk_.resize((size_t)std::max(tail_chunks_, bounce_chunks_));
     for (auto& e : ev_dchunk_) check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
     ev_ready_.resize((size_t)R_);
     ev_free_.resize((size_t)R_);
@@ -742,11 +745,12 @@ void SlabContext::finish(float* host_volume, bp_gpu_stats* st) {
         host_volume = h_bounce_;
     }
     std::vector<std::pair<size_t, size_t>> chunks;  // (offset, count) of the D2H copies
-    if (host_volume && !pending_.empty() && tiled_ && tail_chunks_ > 1 && nz_ >= 2 * ts_.bz) {
+    const int tail_chunks = bounce ? bounce_chunks_ : tail_chunks_;
+    if (host_volume && !pending_.empty() && tiled_ && tail_chunks > 1 && nz_ >= 2 * ts_.bz) {
         // chunk-major tail: for each z-chunk run all deferred batches (ascending
         // view order per voxel is preserved), then stream that chunk back while the
         // next chunk computes
-        const int C = std::min(tail_chunks_, nz_ / ts_.bz);
+        const int C = std::min(tail_chunks, nz_ / ts_.bz);
         std::vector<int> zb((size_t)C + 1);
         for (int c = 0; c <= C; ++c) zb[(size_t)c] = (int)((long long)nz_ * c / C / ts_.bz) * ts_.bz;
         zb[(size_t)C] = nz_;

@@ -148,7 +148,7 @@ private:
     // volume is read back, processed z-chunk-major so each finished chunk's D2H
     // overlaps the next chunk's kernels
     std::vector<Pending> pending_;
-    int tail_batches_ = 3, tail_chunks_ = 8;
+    int tail_batches_ = 3, tail_chunks_ = 8, bounce_chunks_ = 16;
     uint64_t batch_index_ = 0;
     cudaStream_t s_d2h_ = nullptr;
     std::vector<cudaEvent_t> ev_chunk_;
