@@ -688,7 +688,9 @@ def main():
     ap.add_argument("--views", type=int, default=496)
     ap.add_argument("--batch", type=int, default=248, help="views per launch, resident (value) run "
                     "(496 = 2 x 248)")
-    ap.add_argument("--e2e-batch", type=int, default=32, help="views per launch, streamed e2e run")
+    ap.add_argument("--e2e-batch", type=int, default=0,
+                    help="views per launch, streamed e2e run (default 32 for the whole volume, 62 for "
+                         "a z-slab of a multi-GPU run: tools/scaling_projection.py)")
     ap.add_argument("--seed", type=int, default=20110428)
     ap.add_argument("--strict", action="store_true", help="bitwise reference arithmetic")
     ap.add_argument("--cpu-views", type=int, default=64,
@@ -711,6 +713,8 @@ def main():
                     help="N>1: compare rank 0's gathered volume with a single-context run")
     args = ap.parse_args()
     args.fast_off = args.strict
+    if args.e2e_batch <= 0:
+        args.e2e_batch = 32 if int(os.environ.get("WORLD_SIZE", "1")) == 1 else 62
     if args.write_stack:
         return write_stack(args)
     if args.impl == "reference":

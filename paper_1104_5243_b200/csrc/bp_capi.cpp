@@ -573,6 +573,29 @@ int bp_partition_slabs(const double* matrices, int count, uint32_t isx, uint32_t
     });
 }
 
+int bp_slab_work(const double* matrices, int count, uint32_t isx, uint32_t isy, uint32_t l,
+                 const double offset_mm[3], double* work) {
+    if (!matrices || !work || count < 1) return fail(BP_EINVAL, "null argument");
+    return guarded([&] {
+        std::vector<bph::Mat> m((size_t)count);
+        for (int k = 0; k < count; ++k) std::memcpy(m[(size_t)k].data(), matrices + 12 * k, 96);
+        const double* o = offset_mm;
+        auto g = bph::Grid::cube((int)l, o ? o[0] : 0, o ? o[1] : 0, o ? o[2] : 0);
+        std::vector<double> w;
+        bph::partition_slabs(m, (int)isx, (int)isy, g, 1, &w);
+        std::copy(w.begin(), w.end(), work);
+    });
+}
+
+int bp_partition_by_cost(const double* slice_cost, uint32_t l, int G, int align, int* bounds) {
+    if (!slice_cost || !bounds) return fail(BP_EINVAL, "null argument");
+    return guarded([&] {
+        std::vector<double> c(slice_cost, slice_cost + l);
+        auto b = bph::partition_by_cost(c, G, align);
+        std::copy(b.begin(), b.end(), bounds);
+    });
+}
+
 int bp_slab_row_window(const double matrix[12], uint32_t isy, uint32_t l, const double offset_mm[3],
                        int z_begin, int z_end, int* r0, int* r1) {
     if (!matrix || !r0 || !r1) return fail(BP_EINVAL, "null argument");

@@ -336,6 +336,33 @@ void row_window(const Mat& a, const Grid& g, int x0, int x1, int y0, int y1, int
     *r1 = (int)a1;
 }
 
+std::vector<int> partition_by_cost(const std::vector<double>& work, int G, int align) {
+    const int L = (int)work.size();
+    if (G < 1) throw config_error("slab count must be >= 1");
+    if (G > L) throw config_error("more slabs than z-slices");
+    align = std::max(1, align);
+    std::vector<double> cum((size_t)L + 1, 0.0);
+    for (int z = 0; z < L; ++z) {
+        if (!(work[(size_t)z] >= 0)) throw config_error("slice cost must be >= 0");
+        cum[(size_t)z + 1] = cum[(size_t)z] + work[(size_t)z];
+    }
+    const double total = cum[(size_t)L];
+    std::vector<int> b((size_t)G + 1, 0);
+    b[0] = 0;
+    b[(size_t)G] = L;
+    for (int i = 1; i < G; ++i) {
+        const double target = total * i / G;
+        int z = (int)(std::lower_bound(cum.begin(), cum.end(), target) - cum.begin());
+        // pick the closer of z-1, z
+        if (z > 0 && std::fabs(cum[(size_t)z - 1] - target) < std::fabs(cum[(size_t)z] - target)) --z;
+        z = (int)std::lround((double)z / align) * align;
+        z = std::max(z, b[(size_t)i - 1] + 1);
+        z = std::min(z, L - (G - i));
+        b[(size_t)i] = z;
+    }
+    return b;
+}
+
 std::vector<int> partition_slabs(const std::vector<Mat>& mats, int isx, int isy, const Grid& g,
                                  int G, std::vector<double>* work_out) {
     const int L = g.L;
@@ -396,24 +423,9 @@ std::vector<int> partition_slabs(const std::vector<Mat>& mats, int isx, int isy,
     const double rmw = (double)nbx * BX * nby * BY * 0.02;  // volume read/write per slice
     std::vector<double> work((size_t)L, 0.0);
     for (int z = 0; z < L; ++z) work[(size_t)z] = layer[(size_t)(z / BZ)] * per_pair + rmw + 1e-3;
-    std::vector<double> cum((size_t)L + 1, 0.0);
-    for (int z = 0; z < L; ++z) cum[(size_t)z + 1] = cum[(size_t)z] + work[(size_t)z];
-    const double total = cum[(size_t)L];
     // slab bounds on block-layer boundaries when the slabs are thick enough
     const int align = (L / G >= 4 * BZ) ? BZ : 1;
-    std::vector<int> b((size_t)G + 1, 0);
-    b[0] = 0;
-    b[(size_t)G] = L;
-    for (int i = 1; i < G; ++i) {
-        const double target = total * i / G;
-        int z = (int)(std::lower_bound(cum.begin(), cum.end(), target) - cum.begin());
-        // pick the closer of z-1, z
-        if (z > 0 && std::fabs(cum[(size_t)z - 1] - target) < std::fabs(cum[(size_t)z] - target)) --z;
-        z = (int)std::lround((double)z / align) * align;
-        z = std::max(z, b[(size_t)i - 1] + 1);
-        z = std::min(z, L - (G - i));
-        b[(size_t)i] = z;
-    }
+    std::vector<int> b = partition_by_cost(work, G, align);
     if (work_out) *work_out = work;
     return b;
 }

@@ -101,6 +101,8 @@ void row_window(const Mat& a, const Grid& g, int x0, int x1, int y0, int y1, int
 // The work estimate samples voxels on a coarse lattice and views with a stride
 // (a contiguous analogue of the reference's cyclic z scheduling,
 // scheduler.cpp:12-22).  Deterministic.
+// Contiguous slab bounds (G+1) balancing a per-slice cost, bounds on multiples of align.
+std::vector<int> partition_by_cost(const std::vector<double>& work, int G, int align);
 std::vector<int> partition_slabs(const std::vector<Mat>& mats, int isx, int isy, const Grid& g,
                                  int G, std::vector<double>* work_out = nullptr);
 

@@ -150,6 +150,28 @@ def test_partition_is_a_balanced_cover(L, G):
     assert vis.max() / vis.mean() <= max(1.12, vis_eq.max() / vis_eq.mean() + 1e-9)
 
 
+def test_partition_by_cost_balances_any_cost():
+    # uniform cost -> equal slabs on the alignment grid; the model partition equals the
+    # by-cost partition of the model's own per-slice cost (bp_slab_work)
+    b = bp.partition_by_cost(np.ones(1024), 8, 8)
+    assert list(b) == [0, 128, 256, 384, 512, 640, 768, 896, 1024]
+    c = np.r_[np.full(100, 3.0), np.full(156, 1.0)]
+    b = bp.partition_by_cost(c, 2, 1)
+    assert b[0] == 0 and b[-1] == 256 and abs(c[:b[1]].sum() - c[b[1]:].sum()) <= 3.0
+    b = bp.partition_by_cost(np.zeros(16), 16, 1)  # degenerate cost still gives a cover
+    assert list(b) == list(range(17))
+    with pytest.raises(bp.BPError):
+        bp.partition_by_cost(np.ones(8), 9, 1)
+    px, mats = baseline_small(n_views=32, shrink=8, filter=0)
+    L = 128
+    w = bp.slab_work(mats, px.shape[2], px.shape[1], L)
+    assert w.shape == (L,) and np.all(w > 0)
+    for G in (2, 4):
+        align = 4 if L // G >= 16 else 1
+        assert list(bp.partition_slabs(mats, px.shape[2], px.shape[1], L, G)) == \
+            list(bp.partition_by_cost(w, G, align))
+
+
 def test_row_window_is_conservative():
     # a slab reconstructed from ONLY its row window (other rows zeroed) is bitwise
     # identical to the full-detector result: the window holds every footprint

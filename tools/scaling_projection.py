@@ -10,9 +10,9 @@ A G-GPU run takes as long as its slowest slab (each GPU has its own PCIe link on
 8 x B200 box), plus the fused slab gather (the final kernel stores into rank 0's volume
 over NVLink; not modelled). Efficiency = T1 / (G * max_g T_g).
 Usage: python tools/scaling_projection.py [L=1024]
-Env: E2E_BATCH (views per launch of a z-slab's streamed run when G > 1; default 124: with
-row windows a slab uploads ~20-30% of each view, so a larger batch costs little fill time
-and saves volume read-modify-write passes), VERBOSE=1 (per-slab times)."""
+Env: GS (slab counts, default 1,2,4,8), E2E_BATCH (views per launch of a z-slab's streamed run when G > 1; default 62, the
+measured best of 32/62/124 at 1024^3, G = 8: with 124 and the 5-batch deferred tail every
+batch is deferred and the slab's upload no longer overlaps its compute), VERBOSE=1 (per-slab times)."""
 import os, sys, time
 sys.path.insert(0, ".")
 import paper_1104_5243_b200 as bp
@@ -22,13 +22,14 @@ s = bp.Stack.baseline(n_views=496, isx=1248, isy=960)
 px, mats = s.pixels, s.matrices
 n = 496
 B = 248 if L < 2048 else 124
-EB = int(os.environ.get("E2E_BATCH", "124"))
+EB = int(os.environ.get("E2E_BATCH", "62"))
 verbose = os.environ.get("VERBOSE") == "1"
 res, e2e = {}, {}
 host = bp.Volume.create(L)  # one pinned host volume; each slab reads back into its part
 print(f"| G | slab bounds | slowest slab, resident ms | projected resident efficiency | slowest slab, e2e ms | projected e2e efficiency |")
 print("|---|---|---|---|---|---|")
-for G in (1, 2, 4, 8):
+GS = [int(g) for g in os.environ.get("GS", "1,2,4,8").split(",")]
+for G in GS:
     bounds = [int(b) for b in bp.partition_slabs(mats, 1248, 960, L, G)] if G > 1 else [0, L]
     tr, te = [], []
     for g in range(G):
@@ -39,7 +40,7 @@ for G in (1, 2, 4, 8):
             c.time_resident(1)
             tr.append(min(c.time_resident(1)[0] for _ in range(2)))
         out = host.data[z0:z1]
-        eb = 32 if G == 1 else EB
+        eb = 32 if G == 1 else EB  # G = 1: the bench's whole-volume batch
         with bp.GpuContext(L, 1248, 960, device=0, z_begin=z0, z_end=z1, strict=False, view_batch=eb) as c:
             c.backproject_stack(s)
             c.finish(out=out)
@@ -54,5 +55,8 @@ for G in (1, 2, 4, 8):
             print(f"  G={G} slab [{z0},{z1}): resident {tr[-1]:.1f} ms, e2e {te[-1]:.1f} ms (batch {eb})",
                   flush=True)
     res[G], e2e[G] = max(tr), max(te)
-    print(f"| {G} | {bounds} | {res[G]:.1f} | {res[1] / (G * res[G]):.3f} | {e2e[G]:.1f} | "
-          f"{e2e[1] / (G * e2e[G]):.3f} |", flush=True)
+    if 1 in res:
+        print(f"| {G} | {bounds} | {res[G]:.1f} | {res[1] / (G * res[G]):.3f} | {e2e[G]:.1f} | "
+              f"{e2e[1] / (G * e2e[G]):.3f} |", flush=True)
+    else:
+        print(f"| {G} | {bounds} | {res[G]:.1f} | - | {e2e[G]:.1f} | - |", flush=True)
