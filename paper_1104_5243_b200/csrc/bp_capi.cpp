@@ -769,6 +769,10 @@ int bp_reconstruct(const bp_stack* s, const bp_recon_params* p, bp_volume** out,
         // supplies the clip_stats the reference reports.
         bool have_table = false;
         uint64_t table_total = 0;
+        // every matrix against the grid first (w > 0 at the 8 corners, geometry.cpp:130-144):
+        // BP_EVERIFY before any clip-table work, as the reference's validation precedes its
+        // precompute (scheduler.cpp:31-35)
+        for (const auto& m : s->s.mats) bph::validate_matrix_for_grid(m, grid);
         if (p->clip && p->clip_cache) {
             std::ifstream probe(p->clip_cache, std::ios::binary);
             if (probe.good()) {
@@ -783,7 +787,13 @@ int bp_reconstruct(const bp_stack* s, const bp_recon_params* p, bp_volume** out,
                 t.n_views = s->s.count();
                 t.ranges.resize((size_t)2 * t.n_views * p->l * p->l);
                 const int rc = bp_gpu_clip_table(s, p->l, nullptr, t.ranges.data(), &table_total);
-                if (rc != BP_OK) throw bph::device_error(g_last_error);
+                if (rc != BP_OK) {
+                    const std::string m = g_last_error;
+                    if (rc == BP_EINVAL) throw bph::config_error(m);
+                    if (rc == BP_EVERIFY) throw bph::validation_error(m);
+                    if (rc == BP_EIO) throw bph::io_error(m);
+                    throw bph::device_error(m);
+                }
                 bph::write_clip_table(p->clip_cache, t);
             }
             have_table = true;

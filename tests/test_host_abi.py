@@ -172,6 +172,19 @@ def test_partition_by_cost_balances_any_cost():
             list(bp.partition_by_cost(w, G, align))
 
 
+def test_invalid_geometry_is_everify_before_any_clip_work(tmp_path):
+    # validation precedes the clip-table build (scheduler.cpp:31-35): BP_EVERIFY, and no
+    # cache file is written -- on a CPU-only host too (no device work is attempted)
+    px, mats = small_stack("point", 2, 24, 24)
+    bad = mats.copy()
+    bad[1] = [1, 0, 0, 0, 1, 0, 0, 0, 0, 0, 0, -1]
+    cache = str(tmp_path / "c.bpct")
+    with pytest.raises(bp.BPError) as e:
+        bp.reconstruct(bp.Stack.from_arrays(px, bad), bp.recon_params(8, clip=1, clip_cache=cache))
+    assert e.value.code == bp.BP_EVERIFY
+    assert not os.path.exists(cache)
+
+
 def test_row_window_is_conservative():
     # a slab reconstructed from ONLY its row window (other rows zeroed) is bitwise
     # identical to the full-detector result: the window holds every footprint
