@@ -457,8 +457,11 @@ def run_ours(args):
         hctx.close()
 
     # ---- e2e: streamed through the C ABI from pinned host memory ---------------
+    # views=n: the caller knows its view count (a RabbitCT-style harness does), so the
+    # library uploads the last ~112 views band-ordered and reads z-chunks back under the
+    # remaining upload (bp_gpu_config.views)
     e2e_ctx = bp.GpuContext(L, isx, isy, device=device, z_begin=z0, z_end=z1,
-                            strict=args.strict, view_batch=args.e2e_batch)
+                            strict=args.strict, view_batch=args.e2e_batch, views=n)
     host_vol = bp.Volume.create(L)  # pinned (library pool); each rank reads back its slab
     out = host_vol.data[z0:z1]
     for _ in range(max(1, args.warmup)):
@@ -495,7 +498,8 @@ def run_ours(args):
         pg_px = np.array(px, copy=True)  # pageable (numpy heap), not the library's pinned pool
         pg_vol = np.empty((L, L, L), np.float32)
         pg_vol.fill(0.0)
-        cctx = bp.GpuContext(L, isx, isy, device=device, strict=args.strict, view_batch=args.e2e_batch)
+        cctx = bp.GpuContext(L, isx, isy, device=device, strict=args.strict, view_batch=args.e2e_batch,
+                             views=n)
         for _ in range(max(1, min(2, args.warmup))):
             for k in range(n):
                 cctx.backproject(pg_px[k], mats[k], copy=True)

@@ -64,7 +64,7 @@ class GpuConfig(C.Structure):
                 ("kernel", C.c_int), ("count_visible", C.c_int), ("profile_launches", C.c_int),
                 ("recip_mode", C.c_int), ("device_volume", C.c_void_p), ("filter", C.c_int),
                 ("sid_mm", C.c_double), ("sdd_mm", C.c_double), ("pitch_mm", C.c_double),
-                ("output_volume", C.c_void_p), ("tail_batches", C.c_int)]
+                ("output_volume", C.c_void_p), ("tail_batches", C.c_int), ("views", C.c_int)]
 
 
 class GpuStats(C.Structure):
@@ -546,7 +546,7 @@ class GpuContext:
                  view_batch=32, ring_batches=0, strict=True, distance_weight=True,
                  row_windows=True, kernel=0, count_visible=False, profile_launches=False,
                  recip_mode=0, device_volume=None, filter=None, output_volume=None,
-                 tail_batches=-1):
+                 tail_batches=-1, views=0):
         cfg = GpuConfig()
         lib().bp_gpu_config_init(C.byref(cfg))
         cfg.l, cfg.isx, cfg.isy = l, isx, isy
@@ -569,6 +569,7 @@ class GpuContext:
         cfg.recip_mode = recip_mode
         cfg.device_volume = device_volume
         cfg.tail_batches = tail_batches
+        cfg.views = views  # views per reconstruction, if known: band-ordered tail (bp_gpu.h)
         self.l, self.isx, self.isy = l, isx, isy
         self.z_begin, self.z_end = z_begin, (z_end if z_end > 0 else l)
         h = C.c_void_p()

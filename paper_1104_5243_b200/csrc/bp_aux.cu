@@ -203,7 +203,7 @@ int launch_clip_count(const SlabArgs& s, const BatchArgs& b, void* stream) {
 // registers fit beside two resident backprojection CTAs, so the expansion of the
 // next batch runs on a low-priority stream under the current batch's kernel.
 __global__ void __launch_bounds__(128) bp_expand_kernel(const __grid_constant__ ExpandArgs a) {
-    const int e = blockIdx.x;
+    const int e = a.e0 + (int)blockIdx.x;
     const size_t slot = (size_t)a.slot[blockIdx.y];
     const float* img = a.ring + slot * a.isy * a.pitch;
     const float4* up = reinterpret_cast<const float4*>(img + (size_t)(e - 1) * a.pitch);
@@ -260,7 +260,8 @@ int launch_expand_small(const ExpandArgs& a, int n, int blocks, void* stream) {
 int launch_expand(const ExpandArgs& a, int n, void* stream) {
     if (n < 1) return 0;
     if (a.pitch % 4 || a.pitchx < a.pitch) return (int)cudaErrorInvalidValue;
-    dim3 grid((unsigned)(a.isy + 1), (unsigned)n);
+    if (a.e1 > a.e0 && (a.e0 < 0 || a.e1 > a.isy + 1)) return (int)cudaErrorInvalidValue;
+    dim3 grid((unsigned)(a.e1 > a.e0 ? a.e1 - a.e0 : a.isy + 1), (unsigned)n);
     static const bool carve = [] {
         // same shared-memory carveout as the backprojection kernel, so expansion
         // blocks can be co-resident with it on an SM

@@ -57,7 +57,7 @@ int guarded(Fn&& fn) {
 // alive between calls so that repeated reconstructions pay neither cudaMalloc
 // of the volume / projection ring nor stream creation.
 using CtxKey = std::tuple<int, uint32_t, uint32_t, uint32_t, double, double, double, int, int, int,
-                          int, int, int, int, int, int, int, double, double, double>;
+                          int, int, int, int, int, int, int, double, double, double, int>;
 
 // Idle contexts, most recently released first.  Bounded by entry count and by the
 // device memory they hold (BP_CTX_CACHE_MB, default 16 GiB), least recently used
@@ -86,7 +86,8 @@ CtxKey key_of(const bp_gpu_config& c) {
     return CtxKey{c.device,        c.l,           c.isx,         c.isy,        c.offset_mm[0],
                   c.offset_mm[1],  c.offset_mm[2], c.z_begin,     c.z_end,      c.view_batch,
                   c.strict_mode,   c.distance_weight, c.row_windows, c.kernel, c.count_visible,
-                  c.recip_mode,    c.filter,      c.sid_mm,      c.sdd_mm,     c.pitch_mm};
+                  c.recip_mode,    c.filter,      c.sid_mm,      c.sdd_mm,     c.pitch_mm,
+                  c.views};
 }
 
 // Removes every idle context (of `device`, or all when device < 0); the contexts are
@@ -669,6 +670,7 @@ int bp_reconstruct_ex(const bp_stack* s, uint32_t l, const bp_recon_ex* p, float
                     c.sid_mm = p->sid_mm;
                     c.sdd_mm = p->sdd_mm;
                     c.pitch_mm = p->pitch_mm;
+                    c.views = s->s.count();  // the whole stack is at hand: band-ordered tail
                     auto ctx = acquire(c);
                     for (int k = 0; k < s->s.count(); ++k)
                         ctx->backproject(s->s.image(k), s->s.mats[(size_t)k].data(), false);

@@ -80,6 +80,7 @@ struct ExpandArgs {
     const float* ring;
     float2* ringx;
     int isx, isy, pitch, pitchx;  // pitch, pitchx: multiples of 4 (floats / float2)
+    int e0, e1;                   // pair rows [e0, e1) (launch_expand); e1 <= e0: all, 0..isy
     int slot[kMaxBatch];
 };
 int launch_expand(const ExpandArgs& a, int n, void* stream);

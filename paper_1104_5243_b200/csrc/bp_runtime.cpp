@@ -260,7 +260,13 @@ void SlabContext::init() {
     // multi-GPU split uploads only its row windows, so its upload ends well before its
     // compute and 5 deferred batches hide more of its readback (1024^3, outer slab of 8:
     // 60.6 -> 55.7 ms; the whole volume at 512^3 prefers 3: 53.5 vs 59.2 ms)
-    const int tail_default = (z1_ - z0_ < L_) ? 5 : 3;
+    // With the view count known (cfg.views), the deferred tail is the band tail: its
+    // ~112-128 views' rows are uploaded band-ordered at finish, so its chunks complete and
+    // read back under the remaining upload (512^3: 53.5 -> 48.5 ms; 3 / 4 / 5 batches of 32
+    // measured 50.7 / 48.5 / 48.6 ms)
+    const int tail_default = cfg.views > 0 && !cfg.filter ? std::max(1, (112 + B_ / 2) / B_)
+                             : (z1_ - z0_ < L_)          ? 5
+                                                          : 3;
     tail_batches_ = std::max(0, std::min(R_ - 2, cfg.tail_batches >= 0 ? cfg.tail_batches : tail_default));
     tail_chunks_ = 8;
     // a pageable destination adds a host copy per chunk after its D2H; smaller chunks
@@ -308,10 +314,28 @@ void SlabContext::init() {
     if (const char* e = std::getenv("BP_NO_OVERLAP_EXPAND")) overlap_expand_ = std::atoi(e) == 0;
     check(cudaStreamCreateWithFlags(&s_copy_, cudaStreamNonBlocking), "stream");
     check(cudaStreamCreateWithFlags(&s_d2h_, cudaStreamNonBlocking), "stream");
-    ev_chunk_.resize((size_t)std::max(tail_chunks_, bounce_chunks_));
-    for (auto& e : ev_chunk_) check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
-    ev_dchunk_.resize((size_t)std::max(tail_chunks_, bounce_chunks_));
-    for (auto& e : ev_dchunk_) check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+    // BP_BAND_TRACE=1: timing events for the band-tail diagnostics
+    const unsigned trace_flags = std::getenv("BP_BAND_TRACE") ? cudaEventDefault : cudaEventDisableTiming;
+    ev_chunk_.resize((size_t)std::max({tail_chunks_, bounce_chunks_, 32}));
+    for (auto& e : ev_chunk_) check(cudaEventCreateWithFlags(&e, trace_flags), "event");
+    ev_dchunk_.resize((size_t)std::max({tail_chunks_, bounce_chunks_, 32}));
+    for (auto& e : ev_dchunk_) check(cudaEventCreateWithFlags(&e, trace_flags), "event");
+    band_chunks_ = (int)std::min<size_t>(12, ev_chunk_.size());  // 8 / 12 / 16: 48.8 / 48.5 / 48.6 ms
+    if (const char* e = std::getenv("BP_BAND_CHUNKS"))
+        band_chunks_ = std::max(1, std::min((int)ev_chunk_.size(), std::atoi(e)));
+    ev_band_.resize((size_t)band_chunks_);
+    for (auto& e : ev_band_) check(cudaEventCreateWithFlags(&e, trace_flags), "event");
+    check(cudaEventCreateWithFlags(&ev_band_pre_, trace_flags), "event");
+    band_img_.assign((size_t)slots_, nullptr);
+    band_r0_.assign((size_t)slots_, 0);
+    band_r1_.assign((size_t)slots_, 0);
+    band_m_.assign((size_t)slots_, bph::Mat{});
+    // the last tail_batches_ batches of a cfg.views-view reconstruction form the band tail
+    // (BP_NO_BAND=1: off, for A/B)
+    if (cfg.views > 0 && tail_batches_ > 0 && !cfg.filter && !std::getenv("BP_NO_BAND")) {
+        const int nbatch = (cfg.views + B_ - 1) / B_;
+        band_start_ = std::max(0, nbatch - tail_batches_) * B_;
+    }
     ev_ready_.resize((size_t)R_);
     ev_free_.resize((size_t)R_);
     ev_prep_.resize((size_t)R_);
@@ -340,6 +364,8 @@ void SlabContext::release_all() noexcept {
     if (s_d2h_) cudaStreamSynchronize(s_d2h_);
     for (auto e : ev_chunk_) if (e) cudaEventDestroy(e);
     for (auto e : ev_dchunk_) if (e) cudaEventDestroy(e);
+    for (auto e : ev_band_) if (e) cudaEventDestroy(e);
+    if (ev_band_pre_) cudaEventDestroy(ev_band_pre_);
     for (auto e : ev_ready_) if (e) cudaEventDestroy(e);
     for (auto e : ev_free_) if (e) cudaEventDestroy(e);
     for (auto e : ev_prep_) if (e) cudaEventDestroy(e);
@@ -420,6 +446,12 @@ void SlabContext::backproject(const float* image, const double* A, bool copy) {
         if (((r1 - r0) & 1) && r1 < isy_) ++r1;
     }
     const int slot = rg_ * B_ + nb_;
+    const bool withhold = band_start_ >= 0 && views_ >= (uint64_t)band_start_;
+    if (withhold) {
+        band_img_[(size_t)slot] = nullptr;
+        band_r0_[(size_t)slot] = band_r1_[(size_t)slot] = 0;
+        band_m_[(size_t)slot] = m;
+    }
     if (r1 > r0) {
         const float* src = image + (size_t)r0 * isx_;
         if (copy) {
@@ -436,12 +468,18 @@ void SlabContext::backproject(const float* image, const double* A, bool copy) {
             bph::parallel_memcpy(stg, src, (size_t)(r1 - r0) * isx_ * sizeof(float));
             src = stg;
         }
-        if (!any_h2d_) {
+        float* dst = d_ring_ + (size_t)slot * isy_ * pitch_ + (size_t)r0 * pitch_;
+        if (withhold) {
+            // uploaded at finish in row bands (or view-major by upload_withheld)
+            band_img_[(size_t)slot] = reinterpret_cast<const char*>(src) - (size_t)r0 * isx_ * sizeof(float);
+            band_r0_[(size_t)slot] = r0;
+            band_r1_[(size_t)slot] = r1;
+        } else if (!any_h2d_) {
             check(cudaEventRecord(ev_h0_, s_copy_), "event");
             any_h2d_ = true;
         }
-        float* dst = d_ring_ + (size_t)slot * isy_ * pitch_ + (size_t)r0 * pitch_;
-        if (pitch_ == isx_) {
+        if (withhold) {
+        } else if (pitch_ == isx_) {
             // Views whose images are equally spaced in host memory (consecutive images of
             // one stack, or consecutive staging slots) and land in consecutive ring slots
             // form one copy: a plain copy when every window is the full detector, else ONE
@@ -480,7 +518,7 @@ void SlabContext::backproject(const float* image, const double* A, bool copy) {
                                     (size_t)isx_ * sizeof(float), (size_t)isx_ * sizeof(float),
                                     (size_t)(r1 - r0), cudaMemcpyHostToDevice, s_copy_),
                   "H2D");
-        h2d_bytes_ += (uint64_t)(r1 - r0) * isx_ * sizeof(float);
+        if (!withhold) h2d_bytes_ += (uint64_t)(r1 - r0) * isx_ * sizeof(float);
     }
     if (filt_) {
         fr0_[(size_t)nb_] = r1 > r0 ? r0 : 0;
@@ -687,6 +725,7 @@ void SlabContext::launch(const bpg::BatchArgs& b, int zc0, int zc1, bool final_p
 void SlabContext::launch_pending_front(bool final_pass) {
     Pending p = pending_.front();
     pending_.erase(pending_.begin());
+    if (p.band) upload_withheld(p);
     prepare(p);
     check(cudaStreamWaitEvent(s_comp_, p.ready, 0), "wait");
     mark_t0();
@@ -713,6 +752,206 @@ void SlabContext::issue_run() {
     run_n_ = 0;
 }
 
+void SlabContext::copy_rows(const Pending& p, int r0, int r1) {
+    if (r1 <= r0) return;
+    const size_t row = (size_t)isx_ * sizeof(float), view_bytes = row * isy_;
+    const size_t slot_bytes = (size_t)isy_ * pitch_ * sizeof(float);
+    if (!any_h2d_) {
+        check(cudaEventRecord(ev_h0_, s_copy_), "event");
+        any_h2d_ = true;
+    }
+    int i = 0;
+    while (i < p.b.nviews) {
+        const int s0 = p.b.slot[i];
+        const char* img0 = band_img_[(size_t)s0];
+        if (!img0) {
+            ++i;
+            continue;
+        }
+        // a run of views equally spaced in host memory in consecutive slots: one 2-D copy
+        int n = 1;
+        while (pitch_ == isx_ && i + n < p.b.nviews && p.b.slot[i + n] == s0 + n &&
+               band_img_[(size_t)(s0 + n)] == img0 + (size_t)n * view_bytes)
+            ++n;
+        char* dst = reinterpret_cast<char*>(d_ring_) + (size_t)s0 * slot_bytes + (size_t)r0 * pitch_ * sizeof(float);
+        const char* src = img0 + (size_t)r0 * row;
+        if (pitch_ == isx_)
+            check(cudaMemcpy2DAsync(dst, slot_bytes, src, view_bytes, (size_t)(r1 - r0) * row, (size_t)n,
+                                    cudaMemcpyHostToDevice, s_copy_),
+                  "H2D (row band)");
+        else
+            check(cudaMemcpy2DAsync(dst, (size_t)pitch_ * sizeof(float), src, row, row, (size_t)(r1 - r0),
+                                    cudaMemcpyHostToDevice, s_copy_),
+                  "H2D (row band)");
+        h2d_bytes_ += (uint64_t)(r1 - r0) * row * n;
+        i += n;
+    }
+}
+
+void SlabContext::upload_withheld(Pending& p) {
+    if (!p.band) return;
+    Pending one = p;
+    for (int i = 0; i < p.b.nviews; ++i) {
+        const int sl = p.b.slot[i];
+        if (!band_img_[(size_t)sl]) continue;
+        one.b.nviews = 1;
+        one.b.slot[0] = sl;
+        copy_rows(one, band_r0_[(size_t)sl], band_r1_[(size_t)sl]);
+        band_img_[(size_t)sl] = nullptr;
+    }
+    check(cudaEventRecord(ev_ready_[(size_t)p.rg], s_copy_), "event");
+    p.band = false;
+    p.ready = nullptr;
+}
+
+void SlabContext::band_tail(float* host_volume, std::vector<std::pair<size_t, size_t>>& chunks) {
+    // z-chunks on block layers; each one's union row window over the tail's views
+    const int C = std::max(1, std::min(band_chunks_, nz_ / ts_.bz));
+    std::vector<int> zb((size_t)C + 1);
+    for (int c = 0; c <= C; ++c) zb[(size_t)c] = (int)((long long)nz_ * c / C / ts_.bz) * ts_.bz;
+    zb[(size_t)C] = nz_;
+    std::vector<int> lo((size_t)C, isy_), hi((size_t)C, 0);
+    for (const auto& p : pending_)
+        for (int i = 0; i < p.b.nviews; ++i) {
+            const int sl = p.b.slot[i];
+            if (!band_img_[(size_t)sl]) continue;
+            for (int c = 0; c < C; ++c) {
+                int r0 = 0, r1 = 0;
+                bph::row_window(band_m_[(size_t)sl], grid_, 0, L_ - 1, 0, L_ - 1, z0_ + zb[(size_t)c],
+                                z0_ + zb[(size_t)c + 1] - 1, isy_, &r0, &r1);
+                // never beyond the view's own (slab) window, which is all that is staged
+                r0 = std::max(r0, band_r0_[(size_t)sl]);
+                r1 = std::min(r1, band_r1_[(size_t)sl]);
+                if (r1 > r0) {
+                    lo[(size_t)c] = std::min(lo[(size_t)c], r0);
+                    hi[(size_t)c] = std::max(hi[(size_t)c], r1);
+                }
+            }
+        }
+    // outside in: chunks whose rows lie farthest from the detector centre complete first,
+    // so their compute and D2H run while the inner bands are still uploading
+    std::vector<int> order((size_t)C);
+    for (int c = 0; c < C; ++c) order[(size_t)c] = c;
+    auto dist = [&](int c) {
+        if (hi[(size_t)c] <= lo[(size_t)c]) return 1e30;  // reads no rows: first
+        return std::fabs(0.5 * (lo[(size_t)c] + hi[(size_t)c]) - 0.5 * isy_);
+    };
+    std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return dist(a) > dist(b); });
+    // the tail's batches as ONE launch per chunk (ascending view order is kept): one volume
+    // read-modify-write per chunk instead of one per batch, and fewer, fuller waves
+    int total = 0;
+    for (const auto& p : pending_) total += p.b.nviews;
+    std::vector<Pending> tail;
+    if (total <= bpg::kMaxBatch) {
+        Pending m = pending_.front();
+        m.b.nviews = 0;
+        for (const auto& p : pending_)
+            for (int i = 0; i < p.b.nviews; ++i) {
+                m.b.slot[m.b.nviews] = p.b.slot[i];
+                std::memcpy(m.b.A[m.b.nviews], p.b.A[i], sizeof(float) * 12);
+                ++m.b.nviews;
+            }
+        tail.push_back(m);
+    } else {
+        tail = pending_;
+    }
+    // Pair rows (fast mode) are built on the prep stream as soon as their raw rows are in,
+    // each exactly once: pair row e = (p[e-1], p[e] - p[e-1]) (p[-1] = p[isy] = 0) is
+    // built when both raw rows are uploaded.  A voxel at texel row iv reads pair row iv+1,
+    // and a chunk's window holds every in-detector row its voxels read, so every pair row
+    // a chunk reads is built by its own band or an earlier one -- and none is ever
+    // rewritten while a kernel reads it.
+    const bool expd = tiled_ && ts_.dy;
+    const bool trace = std::getenv("BP_BAND_TRACE") != nullptr;
+    if (trace) check(cudaEventRecord(ev_band_pre_, s_copy_), "event");
+    std::vector<char> up((size_t)isy_, 0), built((size_t)isy_ + 1, 0);
+    auto raw_in = [&](int r) { return r < 0 || r >= isy_ || up[(size_t)r]; };
+    for (int k = 0; k < C; ++k) {
+        const int c = order[(size_t)k];
+        int r = lo[(size_t)c];
+        while (r < hi[(size_t)c]) {  // the window's rows not uploaded yet, as runs
+            if (up[(size_t)r]) {
+                ++r;
+                continue;
+            }
+            int e = r;
+            while (e < hi[(size_t)c] && !up[(size_t)e]) up[(size_t)e++] = 1;
+            for (const auto& p : pending_) copy_rows(p, r, e);
+            r = e;
+        }
+        check(cudaEventRecord(ev_band_[(size_t)k], s_copy_), "event");
+        if (expd) {
+            // on the highest-priority stream: the prep stream may still hold the expansions
+            // of the last view-major batches (measured: 3.8 ms of lag behind the copies)
+            mark_t0();
+            check(cudaStreamWaitEvent(s_aux_, ev_t0_, 0), "wait");
+            check(cudaStreamWaitEvent(s_aux_, ev_band_[(size_t)k], 0), "wait");
+            int e = 0;
+            while (e <= isy_) {  // runs of pair rows that just became buildable
+                if (built[(size_t)e] || !raw_in(e - 1) || !raw_in(e)) {
+                    ++e;
+                    continue;
+                }
+                int f = e;
+                while (f <= isy_ && !built[(size_t)f] && raw_in(f - 1) && raw_in(f)) built[(size_t)f++] = 1;
+                for (const auto& p : tail) {
+                    bpg::ExpandArgs a{};
+                    a.ring = d_ring_;
+                    a.ringx = d_ringx_;
+                    a.isx = isx_;
+                    a.isy = isy_;
+                    a.pitch = pitch_;
+                    a.pitchx = pitch_;
+                    a.e0 = e;
+                    a.e1 = f;
+                    for (int i = 0; i < p.b.nviews; ++i) a.slot[i] = p.b.slot[i];
+                    check((cudaError_t)bpg::launch_expand(a, p.b.nviews, s_aux_), "pair ring expansion (band)");
+                    ++prep_launches_;
+                }
+                e = f;
+            }
+            // the chunk's kernels wait on this (its band, and the pair rows built so far)
+            check(cudaEventRecord(ev_band_[(size_t)k], s_aux_), "event");
+        }
+    }
+    mark_t0();
+    for (int k = 0; k < C; ++k) {
+        const int c = order[(size_t)k];
+        check(cudaStreamWaitEvent(s_comp_, ev_band_[(size_t)k], 0), "wait");
+        for (size_t i = 0; i < tail.size(); ++i) {
+            auto p = tail[i];
+            p.b.load_volume = p.index > 0 ? 1 : 0;
+            launch(p.b, zb[(size_t)c], zb[(size_t)c + 1], i + 1 == tail.size());
+        }
+        check(cudaEventRecord(ev_chunk_[(size_t)k], s_comp_), "event");
+        check(cudaStreamWaitEvent(s_d2h_, ev_chunk_[(size_t)k], 0), "wait");
+        if (k == 0) check(cudaEventRecord(ev_d0_, s_d2h_), "event");
+        const size_t off = (size_t)zb[(size_t)c] * L_ * L_;
+        const size_t n = (size_t)(zb[(size_t)c + 1] - zb[(size_t)c]) * L_ * L_;
+        check(cudaMemcpyAsync(host_volume + off, result() + off, n * sizeof(float), cudaMemcpyDefault, s_d2h_),
+              "D2H");
+        check(cudaEventRecord(ev_dchunk_[(size_t)k], s_d2h_), "event");
+        chunks.emplace_back(off, n);
+    }
+    for (const auto& p : pending_)
+        for (int i = 0; i < p.b.nviews; ++i) band_img_[(size_t)p.b.slot[i]] = nullptr;
+    if (trace) {  // diagnostics: per chunk, ms after the first H2D
+        check(cudaDeviceSynchronize(), "sync");
+        auto ms = [&](cudaEvent_t e) {
+            float t = 0;
+            return cudaEventElapsedTime(&t, ev_h0_, e) == cudaSuccess ? t : -1.0f;
+        };
+        std::fprintf(stderr, "band tail: %d views of %d batches; view-major uploads done %7.2f\n", total,
+                     (int)pending_.size(), ms(ev_band_pre_));
+        for (int k = 0; k < C; ++k) {
+            const int c = order[(size_t)k];
+            std::fprintf(stderr, "band chunk %2d z[%4d,%4d) rows[%4d,%4d): uploaded %7.2f computed %7.2f read back %7.2f\n",
+                         k, zb[(size_t)c], zb[(size_t)c + 1], lo[(size_t)c], hi[(size_t)c], ms(ev_band_[(size_t)k]),
+                         ms(ev_chunk_[(size_t)k]), ms(ev_dchunk_[(size_t)k]));
+        }
+    }
+}
+
 void SlabContext::flush() {
     if (nb_ == 0) return;
     issue_run();  // every copy of the batch precedes its ready event
@@ -720,7 +959,9 @@ void SlabContext::flush() {
     choose_tile(cur_);
     check(cudaEventRecord(ev_ready_[(size_t)rg_], s_copy_), "event");
     pending_.push_back(Pending{cur_, rg_, batch_index_++, fr0_, fr1_});
-    prepare(pending_.back());
+    // band_start_ is batch-aligned: a batch is withheld whole or not at all
+    pending_.back().band = band_start_ >= 0 && views_ - (uint64_t)nb_ >= (uint64_t)band_start_;
+    if (!pending_.back().band) prepare(pending_.back());
     rg_ = (rg_ + 1) % R_;
     nb_ = 0;
     while ((int)pending_.size() > tail_batches_) launch_pending_front();
@@ -746,7 +987,22 @@ void SlabContext::finish(float* host_volume, bp_gpu_stats* st) {
     }
     std::vector<std::pair<size_t, size_t>> chunks;  // (offset, count) of the D2H copies
     const int tail_chunks = bounce ? bounce_chunks_ : tail_chunks_;
-    if (host_volume && !pending_.empty() && tiled_ && tail_chunks > 1 && nz_ >= 2 * ts_.bz) {
+    const bool band = host_volume && tiled_ && !pending_.empty() && nz_ >= 2 * ts_.bz &&
+                      std::all_of(pending_.begin(), pending_.end(), [](const Pending& p) { return p.band; });
+    if (!band)
+        for (auto& p : pending_) upload_withheld(p);
+    if (band) {
+        band_tail(host_volume, chunks);
+        any_launch_ = true;
+        for (const auto& p : pending_) {
+            check(cudaEventRecord(ev_free_[(size_t)p.rg], s_comp_), "event");
+            used_[(size_t)p.rg] = true;
+        }
+        pending_.clear();
+        check(cudaEventRecord(ev_t1_, s_comp_), "event");
+        check(cudaEventRecord(ev_d1_, s_d2h_), "event");
+        d2h_done = true;
+    } else if (host_volume && !pending_.empty() && tiled_ && tail_chunks > 1 && nz_ >= 2 * ts_.bz) {
         // chunk-major tail: for each z-chunk run all deferred batches (ascending
         // view order per voxel is preserved), then stream that chunk back while the
         // next chunk computes

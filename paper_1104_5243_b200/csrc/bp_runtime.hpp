@@ -88,6 +88,7 @@ private:
         std::array<int, bpg::kMaxBatch> fr0, fr1;  // rows to filter per view (cfg_.filter)
         bool filtered = false;
         bool expanded = false;
+        bool band = false;  // its views' uploads are withheld (band tail, cfg_.views)
         cudaEvent_t ready = nullptr;  // the batch's inputs are final (uploaded + prepared)
     };
     // FDK filter and pair-ring expansion of a batch on the low-priority prep stream,
@@ -102,6 +103,12 @@ private:
     void launch_pending_front(bool final_pass = false);
     void reset_recon();
     void issue_run();  // pending coalesced H2D copy
+    // band tail (cfg_.views > 0): a batch whose uploads were withheld gets
+    // them view-major (when it must be launched before finish); or finish issues the whole
+    // tail in detector-row bands, z-chunks outside in, each chunk read back as it completes
+    void upload_withheld(Pending& p);
+    void band_tail(float* host_volume, std::vector<std::pair<size_t, size_t>>& chunks);
+    void copy_rows(const Pending& p, int r0, int r1);  // rows [r0, r1) of a band batch's views
     void mark_t0();  // first compute-stream work of a reconstruction
 
     bp_gpu_config cfg_;
@@ -155,6 +162,15 @@ private:
     std::vector<cudaEvent_t> ev_dchunk_;  // a chunk's D2H has landed (pageable readback)
     float* h_bounce_ = nullptr;           // pinned bounce for a pageable host volume
     size_t bounce_bytes_ = 0;
+    // band tail: views from band_start_ on are withheld; per ring slot their host image
+    // (row 0), row window and matrix
+    int band_start_ = -1;  // < 0: off
+    int band_chunks_ = 16;
+    std::vector<const char*> band_img_;
+    std::vector<int> band_r0_, band_r1_;
+    std::vector<bph::Mat> band_m_;
+    std::vector<cudaEvent_t> ev_band_;
+    cudaEvent_t ev_band_pre_ = nullptr;  // BP_BAND_TRACE: the view-major uploads are done
 
     // pending H2D run on s_copy_: run_n_ views whose images start at run_img0_ + i * view
     // bytes, into ring slots run_slot0_ + i, rows [run_r0_, run_r1_) (the union of their
