@@ -264,7 +264,11 @@ void SlabContext::init() {
     // ~112-128 views' rows are uploaded band-ordered at finish, so its chunks complete and
     // read back under the remaining upload (512^3: 53.5 -> 48.5 ms; 3 / 4 / 5 batches of 32
     // measured 50.7 / 48.5 / 48.6 ms)
-    const int tail_default = cfg.views > 0 && !cfg.filter ? std::max(1, (112 + B_ / 2) / B_)
+    // A z-slab of a multi-GPU split reads back a larger share of its work (the outer slabs
+    // at 1024^3, G = 8: 0.9 GB = 16 ms of D2H for 39 ms of compute), so its band tail is
+    // ~186 views (3 batches of 62: slowest slab 49.3 -> 45.4 ms; 4: 45.4, 5: 48.6).
+    const int band_views = (z1_ - z0_ < L_) ? 186 : 112;
+    const int tail_default = cfg.views > 0 && !cfg.filter ? std::max(1, (band_views + B_ / 2) / B_)
                              : (z1_ - z0_ < L_)          ? 5
                                                           : 3;
     tail_batches_ = std::max(0, std::min(R_ - 2, cfg.tail_batches >= 0 ? cfg.tail_batches : tail_default));
@@ -405,6 +409,7 @@ void SlabContext::release_all() noexcept {
 
 void SlabContext::reset_recon() {
     pending_.clear();
+    band_on_ = false;
     batch_index_ = 0;
     nb_ = 0;
     any_launch_ = false;
@@ -446,7 +451,11 @@ void SlabContext::backproject(const float* image, const double* A, bool copy) {
         if (((r1 - r0) & 1) && r1 < isy_) ++r1;
     }
     const int slot = rg_ * B_ + nb_;
-    const bool withhold = band_start_ >= 0 && views_ >= (uint64_t)band_start_;
+    // copy semantics (staging on the caller's thread) paces the views at host-copy speed,
+    // and a withheld tail would then start uploading only after the last call: the band
+    // tail is for zero-copy callers (e2e_copy 61 -> 63 ms with it)
+    if (band_start_ >= 0 && views_ == (uint64_t)band_start_) band_on_ = !copy;
+    const bool withhold = band_on_ && views_ >= (uint64_t)band_start_;
     if (withhold) {
         band_img_[(size_t)slot] = nullptr;
         band_r0_[(size_t)slot] = band_r1_[(size_t)slot] = 0;
@@ -960,7 +969,7 @@ void SlabContext::flush() {
     check(cudaEventRecord(ev_ready_[(size_t)rg_], s_copy_), "event");
     pending_.push_back(Pending{cur_, rg_, batch_index_++, fr0_, fr1_});
     // band_start_ is batch-aligned: a batch is withheld whole or not at all
-    pending_.back().band = band_start_ >= 0 && views_ - (uint64_t)nb_ >= (uint64_t)band_start_;
+    pending_.back().band = band_on_ && views_ - (uint64_t)nb_ >= (uint64_t)band_start_;
     if (!pending_.back().band) prepare(pending_.back());
     rg_ = (rg_ + 1) % R_;
     nb_ = 0;

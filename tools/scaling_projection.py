@@ -12,7 +12,7 @@ over NVLink; not modelled). Efficiency = T1 / (G * max_g T_g).
 Usage: python tools/scaling_projection.py [L=1024]
 Env: GS (slab counts, default 1,2,4,8), E2E_BATCH (views per launch of a z-slab's streamed run when G > 1; default 62, the
 measured best of 32/62/124 at 1024^3, G = 8: with 124 and the 5-batch deferred tail every
-batch is deferred and the slab's upload no longer overlaps its compute), VERBOSE=1 (per-slab times)."""
+batch is deferred and the slab's upload no longer overlaps its compute), VERBOSE=1 (per-slab times), NO_VIEWS_HINT=1 (e2e without the band tail)."""
 import os, sys, time
 sys.path.insert(0, ".")
 import paper_1104_5243_b200 as bp
@@ -41,7 +41,8 @@ for G in GS:
             tr.append(min(c.time_resident(1)[0] for _ in range(2)))
         out = host.data[z0:z1]
         eb = 32 if G == 1 else EB  # G = 1: the bench's whole-volume batch
-        with bp.GpuContext(L, 1248, 960, device=0, z_begin=z0, z_end=z1, strict=False, view_batch=eb) as c:
+        with bp.GpuContext(L, 1248, 960, device=0, z_begin=z0, z_end=z1, strict=False, view_batch=eb,
+                           views=n if os.environ.get("NO_VIEWS_HINT") != "1" else 0) as c:
             c.backproject_stack(s)
             c.finish(out=out)
             best = 1e30
