@@ -335,10 +335,21 @@ void SlabContext::init() {
     band_r1_.assign((size_t)slots_, 0);
     band_m_.assign((size_t)slots_, bph::Mat{});
     // the last tail_batches_ batches of a cfg.views-view reconstruction form the band tail
-    // (BP_NO_BAND=1: off, for A/B)
+    // (BP_NO_BAND=1: off, for A/B).  The tail is settled per reconstruction by its first
+    // call: zero-copy callers get the band tail; copy-semantics callers do not.  Their views
+    // arrive at host-copy pace, and e2e_copy is bound by host DRAM traffic (staging, the
+    // DMA's own reads, the bounce readback and its copy): band tails of 32 / 64 / 96 / 128
+    // views measured 63.5 / 63.0 / 62.5 / 63.8 ms against 62.4 ms without (A/B knob
+    // BP_COPY_BAND_VIEWS, views)
     if (cfg.views > 0 && tail_batches_ > 0 && !cfg.filter && !std::getenv("BP_NO_BAND")) {
-        const int nbatch = (cfg.views + B_ - 1) / B_;
-        band_start_ = std::max(0, nbatch - tail_batches_) * B_;
+        band_tail_zc_ = tail_batches_;
+        int cv = 0;
+        if (const char* e = std::getenv("BP_COPY_BAND_VIEWS")) cv = std::max(0, std::atoi(e));
+        band_tail_copy_ = (cfg.tail_batches >= 0 || std::getenv("BP_TAIL_BATCHES"))
+                              ? tail_batches_
+                              : std::max(1, std::min(tail_batches_, (cv + B_ / 2) / B_));
+        if (cv == 0) band_tail_copy_ = 0;
+        band_start_ = 0;  // set per reconstruction
     }
     ev_ready_.resize((size_t)R_);
     ev_free_.resize((size_t)R_);
@@ -454,7 +465,15 @@ void SlabContext::backproject(const float* image, const double* A, bool copy) {
     // copy semantics (staging on the caller's thread) paces the views at host-copy speed,
     // and a withheld tail would then start uploading only after the last call: the band
     // tail is for zero-copy callers (e2e_copy 61 -> 63 ms with it)
-    if (band_start_ >= 0 && views_ == (uint64_t)band_start_) band_on_ = !copy;
+    if (band_start_ >= 0 && views_ == 0) {  // this reconstruction's tail: by its first call
+        const int t = copy ? band_tail_copy_ : band_tail_zc_;
+        band_on_ = t > 0;
+        tail_batches_ = band_on_ ? t : band_tail_zc_;
+        if (band_on_) {
+            const int nbatch = (cfg_.views + B_ - 1) / B_;
+            band_start_ = std::max(0, nbatch - t) * B_;
+        }
+    }
     const bool withhold = band_on_ && views_ >= (uint64_t)band_start_;
     if (withhold) {
         band_img_[(size_t)slot] = nullptr;

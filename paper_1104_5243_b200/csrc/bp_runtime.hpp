@@ -165,7 +165,8 @@ private:
     // band tail: views from band_start_ on are withheld; per ring slot their host image
     // (row 0), row window and matrix
     int band_start_ = -1;  // < 0: off
-    bool band_on_ = false;  // this reconstruction withholds (its first tail view was zero-copy)
+    bool band_on_ = false;  // this reconstruction withholds its tail
+    int band_tail_zc_ = 0, band_tail_copy_ = 0;  // tail batches for zero-copy / copy callers
     int band_chunks_ = 16;
     std::vector<const char*> band_img_;
     std::vector<int> band_r0_, band_r1_;

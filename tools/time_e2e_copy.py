@@ -1,6 +1,6 @@
 """Wall time of bench.py's e2e_copy leg: bp_gpu_backproject (copy semantics) per view from
 PAGEABLE numpy buffers, bp_gpu_finish into a PAGEABLE volume, next to the pinned zero-copy
-e2e leg.  One library build per run (BP_LIB_PATH).  Env: AB_L (512), AB_BATCH (32), AB_REPS (3), AB_LEG (e2e,e2e_copy), AB_STRICT (0)."""
+e2e leg.  One library build per run (BP_LIB_PATH).  Env: AB_L (512), AB_BATCH (32), AB_REPS (3), AB_LEG (e2e,e2e_copy), AB_STRICT (0), AB_VIEWS (views hint, 496; 0: none)."""
 import os, statistics, sys, time
 import numpy as np
 sys.path.insert(0, ".")
@@ -17,7 +17,8 @@ if "e2e_copy" in legs:
 vol = bp.Volume.create(L)
 res = {}
 with bp.GpuContext(L, 1248, 960, device=0, view_batch=B,
-                   strict=os.environ.get("AB_STRICT") == "1") as c:
+                   strict=os.environ.get("AB_STRICT") == "1",
+                   views=int(os.environ.get("AB_VIEWS", "496"))) as c:
     for leg in legs:
         for r in range(reps + 1):
             t0 = time.perf_counter()
