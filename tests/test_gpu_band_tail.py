@@ -69,3 +69,13 @@ def test_band_tail_copy_pageable_slab_and_repeat():
     assert bitwise_equal(c, ref)
     s = _recon(px, mats, L, 70, strict=True, batch=8, z=(40, 104))[0]
     assert bitwise_equal(s, ref[40:104])
+
+
+def test_band_tail_bitwise_at_1024_whole_and_outer_slab(stack):
+    # config 4: the two-y-row pair kernel, and a z-slab with the 186-view slab tail
+    px, mats = stack.pixels, stack.matrices
+    for z in ((0, 0), (0, 216)):
+        ref = _recon(px, mats, 1024, 0, strict=False, z=z, batch=32 if z == (0, 0) else 62)[0]
+        band = _recon(px, mats, 1024, px.shape[0], strict=False, z=z, batch=32 if z == (0, 0) else 62)[0]
+        assert bitwise_equal(band, ref), z
+        del ref, band
