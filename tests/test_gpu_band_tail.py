@@ -21,12 +21,12 @@ def stack():
 
 
 def _recon(px, mats, L, views_hint, *, strict, batch=32, copy=False, pageable_out=False,
-           z=(0, 0), reps=1):
+           z=(0, 0), reps=1, filt=None):
     isy, isx = px.shape[1], px.shape[2]
     z0, z1 = z
     outs = []
     with bp.GpuContext(L, isx, isy, device=0, strict=strict, view_batch=batch, views=views_hint,
-                       z_begin=z0, z_end=z1) as c:
+                       z_begin=z0, z_end=z1, filter=filt) as c:
         nz = c.z_end - c.z_begin
         for _ in range(reps):
             for k in range(px.shape[0]):
@@ -79,3 +79,14 @@ def test_band_tail_bitwise_at_1024_whole_and_outer_slab(stack):
         band = _recon(px, mats, 1024, px.shape[0], strict=False, z=z, batch=32 if z == (0, 0) else 62)[0]
         assert bitwise_equal(band, ref), z
         del ref, band
+
+
+def test_band_tail_odd_width_and_filter():
+    # an odd detector width (ring pitch != width: per-view band copies) and FDK filtering
+    # (band tail off: filtering needs whole rows per batch) both stay bitwise
+    px, mats = small_stack("spheres3", 60, 250, 200)
+    ref = _recon(px, mats, 128, 0, strict=False, batch=16)[0]
+    assert bitwise_equal(_recon(px, mats, 128, 60, strict=False, batch=16)[0], ref)
+    geom = (750.0, 1200.0, 0.32 * 1248.0 / 250)
+    ref = _recon(px, mats, 128, 0, strict=False, batch=16, filt=geom)[0]
+    assert bitwise_equal(_recon(px, mats, 128, 60, strict=False, batch=16, filt=geom)[0], ref)
