@@ -567,7 +567,7 @@ def run_ours(args):
     if world == 1 and not args.no_fdk:
         geom = (750.0, 1200.0, 0.32 * 1248.0 / isx)
         fctx = bp.GpuContext(L, isx, isy, device=device, strict=args.strict,
-                             view_batch=args.e2e_batch, filter=geom)
+                             view_batch=args.e2e_batch, filter=geom, views=n)
         for _ in range(max(1, args.warmup)):
             fctx.backproject_stack(stack)
             fctx.finish(out=out)

@@ -268,7 +268,7 @@ void SlabContext::init() {
     // at 1024^3, G = 8: 0.9 GB = 16 ms of D2H for 39 ms of compute), so its band tail is
     // ~186 views (3 batches of 62: slowest slab 49.3 -> 45.4 ms; 4: 45.4, 5: 48.6).
     const int band_views = (z1_ - z0_ < L_) ? 186 : 112;
-    const int tail_default = cfg.views > 0 && !cfg.filter ? std::max(1, (band_views + B_ / 2) / B_)
+    const int tail_default = cfg.views > 0 ? std::max(1, (band_views + B_ / 2) / B_)
                              : (z1_ - z0_ < L_)          ? 5
                                                           : 3;
     tail_batches_ = std::max(0, std::min(R_ - 2, cfg.tail_batches >= 0 ? cfg.tail_batches : tail_default));
@@ -341,7 +341,7 @@ void SlabContext::init() {
     // DMA's own reads, the bounce readback and its copy): band tails of 32 / 64 / 96 / 128
     // views measured 63.5 / 63.0 / 62.5 / 63.8 ms against 62.4 ms without (A/B knob
     // BP_COPY_BAND_VIEWS, views)
-    if (cfg.views > 0 && tail_batches_ > 0 && !cfg.filter && !std::getenv("BP_NO_BAND")) {
+    if (cfg.views > 0 && tail_batches_ > 0 && !std::getenv("BP_NO_BAND")) {
         band_tail_zc_ = tail_batches_;
         int cv = 0;
         if (const char* e = std::getenv("BP_COPY_BAND_VIEWS")) cv = std::max(0, std::atoi(e));
@@ -856,6 +856,14 @@ void SlabContext::band_tail(float* host_volume, std::vector<std::pair<size_t, si
                 }
             }
         }
+    // FDK filtering (cfg_.filter) transforms rows (2i, 2i+1) as one complex FFT: band runs
+    // then consist of whole row pairs, so filtering band by band equals filtering whole views
+    if (filt_)
+        for (int c = 0; c < C; ++c)
+            if (hi[(size_t)c] > lo[(size_t)c]) {
+                lo[(size_t)c] &= ~1;
+                hi[(size_t)c] = std::min(isy_, (hi[(size_t)c] + 1) & ~1);
+            }
     // outside in: chunks whose rows lie farthest from the detector centre complete first,
     // so their compute and D2H run while the inner bands are still uploading
     std::vector<int> order((size_t)C);
@@ -894,6 +902,7 @@ void SlabContext::band_tail(float* host_volume, std::vector<std::pair<size_t, si
     if (trace) check(cudaEventRecord(ev_band_pre_, s_copy_), "event");
     std::vector<char> up((size_t)isy_, 0), built((size_t)isy_ + 1, 0);
     auto raw_in = [&](int r) { return r < 0 || r >= isy_ || up[(size_t)r]; };
+    std::vector<std::pair<int, int>> runs;  // this band's newly uploaded rows
     for (int k = 0; k < C; ++k) {
         const int c = order[(size_t)k];
         int r = lo[(size_t)c];
@@ -905,9 +914,29 @@ void SlabContext::band_tail(float* host_volume, std::vector<std::pair<size_t, si
             int e = r;
             while (e < hi[(size_t)c] && !up[(size_t)e]) up[(size_t)e++] = 1;
             for (const auto& p : pending_) copy_rows(p, r, e);
+            runs.emplace_back(r, e);
             r = e;
         }
         check(cudaEventRecord(ev_band_[(size_t)k], s_copy_), "event");
+        if (filt_ && !runs.empty()) {  // the band's new rows, filtered in place
+            mark_t0();
+            check(cudaStreamWaitEvent(s_aux_, ev_t0_, 0), "wait");
+            check(cudaStreamWaitEvent(s_aux_, ev_band_[(size_t)k], 0), "wait");
+            for (const auto& run : runs)
+                for (const auto& p : tail) {
+                    std::array<int, bpg::kMaxBatch> r0s{}, r1s{};
+                    for (int i = 0; i < p.b.nviews; ++i) {
+                        r0s[(size_t)i] = run.first;
+                        r1s[(size_t)i] = run.second;
+                    }
+                    filt_->apply_batch(d_ring_, (long long)isy_ * pitch_, pitch_, p.b.nviews, p.b.slot,
+                                       r0s.data(), r1s.data(), s_aux_);
+                    ++prep_launches_;
+                }
+            runs.clear();
+            check(cudaEventRecord(ev_band_[(size_t)k], s_aux_), "event");
+        }
+        runs.clear();
         if (expd) {
             // on the highest-priority stream: the prep stream may still hold the expansions
             // of the last view-major batches (measured: 3.8 ms of lag behind the copies)

@@ -83,7 +83,7 @@ def test_band_tail_bitwise_at_1024_whole_and_outer_slab(stack):
 
 def test_band_tail_odd_width_and_filter():
     # an odd detector width (ring pitch != width: per-view band copies) and FDK filtering
-    # (band tail off: filtering needs whole rows per batch) both stay bitwise
+    # (band runs of whole row pairs, filtered band by band) both stay bitwise
     px, mats = small_stack("spheres3", 60, 250, 200)
     ref = _recon(px, mats, 128, 0, strict=False, batch=16)[0]
     assert bitwise_equal(_recon(px, mats, 128, 60, strict=False, batch=16)[0], ref)
