@@ -472,9 +472,12 @@ def run_ours(args):
     t0 = time.perf_counter()
     h2d = d2h = 0
     h2d_ms = d2h_ms = 0.0
+    e2e_each = []
     for _ in range(args.steps):
+        t1 = time.perf_counter()
         e2e_ctx.backproject_stack(stack)
         _, est = e2e_ctx.finish(out=out)
+        e2e_each.append((time.perf_counter() - t1) * 1e3)
         h2d += est.h2d_bytes
         d2h += est.d2h_bytes
         h2d_ms += est.h2d_ms
@@ -658,7 +661,8 @@ def run_ours(args):
         "e2e": {"value": e2e_val, "unit": "GUP/s", "h2d_bytes_per_step": h2d // args.steps,
                 "d2h_bytes_per_step": d2h // args.steps,
                 "ms_per_step": e2e_s * 1e3 / args.steps,
-                "h2d_ms_per_step": h2d_ms / args.steps, "d2h_ms_per_step": d2h_ms / args.steps},
+                "h2d_ms_per_step": h2d_ms / args.steps, "d2h_ms_per_step": d2h_ms / args.steps,
+                "ms_each": [round(x, 2) for x in e2e_each]},
         "clocks": clocks,
         "tile": {"w": st.tile_w, "h": st.tile_h, "block": [st.block_x, st.block_y, st.block_z],
                  "tile_pairs": st.tile_pairs, "skipped_pairs": st.skipped_pairs,
