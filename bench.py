@@ -653,11 +653,12 @@ def run_ours(args):
                                  "views: 8-byte pair-ring texels in fast mode, 4-byte raw in strict) / live "
                                  "mean launch time; ncu: profiles/latest.json. HBM is not the bound"},
                      "binding_unit": {
-                         "unit": "co-limit: LSU shared-memory wavefronts (1 per clk per SM) and FMA-pipe issue",
-                         "util": prof.get("lsu_wavefronts_pct", 0.0) / 100.0,
-                         "fma_pipe_util": prof.get("fma_pipe_active_pct", 0.0) / 100.0,
-                         "source": "ncu --set full of the same kernel (profiles/latest.json); at the margin "
-                                   "time follows FMA-pipe work, not conflict replays (DESIGN.md 3.5)"}},
+                         "unit": "FMA pipe at the margin (~19 lane-ops per update with exact coordinates); "
+                                 "LSU shared-memory wavefronts busy but not limiting (DESIGN.md 3.5 A/Bs)",
+                         "util": prof.get("fma_pipe_active_pct", 0.0) / 100.0,
+                         "lsu_wavefront_util": prof.get("lsu_wavefronts_pct", 0.0) / 100.0,
+                         "issue_active": prof.get("issue_active_pct", 0.0) / 100.0,
+                         "source": "ncu --set full of the same kernel (profiles/latest.json)"}},
         "e2e": {"value": e2e_val, "unit": "GUP/s", "h2d_bytes_per_step": h2d // args.steps,
                 "d2h_bytes_per_step": d2h // args.steps,
                 "ms_per_step": e2e_s * 1e3 / args.steps,
