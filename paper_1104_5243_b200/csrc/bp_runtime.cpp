@@ -576,9 +576,10 @@ void SlabContext::choose_tile(const bpg::BatchArgs& b) {
     }
     // fast mode reads the pair ring where a pair variant exists
     t.dy = (!cfg_.strict_mode && pair_ok_ && bpg::has_pair_variant(t)) ? 1 : 0;
-    // x-quads (one y-row of 4 x-voxels per thread) for the pair kernel below 1024^3:
-    // +0.85% at 512^3, -0.55% at 1024^3 and 2048^3 (A/B, 248-view launches)
-    if (t.dy && L_ < 1024 && !std::getenv("BP_NO_XQ")) {
+    // x-quads (one y-row of 4 x-voxels per thread) for the pair kernel: +0.85% at 512^3 in
+    // round 1 (then -0.55% at 1024^3 and 2048^3); with the warp-parallel cull and the SHF
+    // texel addresses of round 2 also +1.4% at 1024^3 and +1.2% at 2048^3 (A/B, BP_NO_XQ=1)
+    if (t.dy && !std::getenv("BP_NO_XQ")) {
         bpg::TileShape q = t;
         q.xp = 2;
         if (bpg::has_pair_variant(q)) t.xp = 2;
