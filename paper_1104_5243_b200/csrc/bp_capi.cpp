@@ -343,7 +343,7 @@ void bp_gpu_config_init(bp_gpu_config* c) {
     if (!c) return;
     std::memset(c, 0, sizeof *c);
     c->device = -1;
-    c->view_batch = 32;
+    c->view_batch = 0;    /* library default: 32; 62 for whole volumes of 1024^3 or more */
     c->ring_batches = 0;  /* library default: 8 batches (tail deferral needs >= 8) */
     c->strict_mode = 1;
     c->distance_weight = 1;
@@ -614,7 +614,7 @@ int bp_slab_row_window(const double matrix[12], uint32_t isy, uint32_t l, const 
 void bp_recon_ex_init(bp_recon_ex* p) {
     if (!p) return;
     std::memset(p, 0, sizeof *p);
-    p->view_batch = 32;
+    p->view_batch = 0;  /* library default (bp_gpu_config.view_batch) */
     p->strict_mode = 1;
     p->distance_weight = 1;
     p->row_windows = 1;
@@ -659,7 +659,7 @@ int bp_reconstruct_ex(const bp_stack* s, uint32_t l, const bp_recon_ex* p, float
                     c.device = devs[(size_t)d];
                     c.z_begin = bounds[(size_t)g];
                     c.z_end = bounds[(size_t)g + 1];
-                    c.view_batch = p->view_batch > 0 ? p->view_batch : 32;
+                    c.view_batch = p->view_batch > 0 ? p->view_batch : 0;
                     c.strict_mode = p->strict_mode;
                     c.distance_weight = p->distance_weight;
                     c.row_windows = p->row_windows;

@@ -252,7 +252,10 @@ void SlabContext::init() {
     isx_ = (int)cfg.isx;
     isy_ = (int)cfg.isy;
     pitch_ = round_up(isx_, 4);  // TMA global strides must be multiples of 16 B
-    B_ = cfg.view_batch > 0 ? cfg.view_batch : 32;
+    // default register batch: 32 views; 62 for a whole volume of 1024^3 or more, whose compute
+    // outlasts its upload, so that halving the volume read-modify-write passes pays
+    // (1024^3 e2e 328 -> 314 ms, A/B profiles/round2_e2e_batch_1024.txt)
+    B_ = cfg.view_batch > 0 ? cfg.view_batch : ((long long)(z1_ - z0_) * L_ * L_ >= (1ll << 30) ? 62 : 32);
     if (B_ > bpg::kMaxBatch) throw bph::config_error("view_batch exceeds 256");
     R_ = cfg.ring_batches > 0 ? cfg.ring_batches : 8;
     // measured on B200 at 512^3 (tools: scratch e2e A/B): deferring 3 batches and

@@ -5,7 +5,7 @@ For each config it reports:
   124 at 2048³);
 - visible GUP/s: clip_stats semantics;
 - e2e ms: pinned host stack in, host volume out, through the C ABI streaming call (view count
-  given: band tail).
+  given: band tail; library-default view batch: 32, 62 from 1024³ up).
 
 Config 5 is the 2048³ grid offset +60 mm in x. Its volume is 32 GB on one GPU here; BASELINE shards it
 over 8 GPUs.
@@ -39,7 +39,7 @@ for L in Ls:
         ms = min(c.time_resident(1)[0] for _ in range(3))
     host = bp.Volume.create(L)  # pinned host volume (32 GB at 2048^3)
     out = host.data
-    with bp.GpuContext(L, 1248, 960, offset=off, strict=False, view_batch=32, views=n) as c:
+    with bp.GpuContext(L, 1248, 960, offset=off, strict=False, view_batch=0, views=n) as c:
         c.backproject_stack(s)
         c.finish(out=out)
         t0 = time.perf_counter()
