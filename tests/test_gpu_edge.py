@@ -50,3 +50,23 @@ def test_context_reused_across_stacks():
                 c.backproject(px[k], m[k], copy=False)
             vol, _ = c.finish()
             assert bitwise_equal(vol, ref)
+
+
+def test_default_view_batch():
+    # view_batch <= 0 selects the library default (bp_gpu.h): 32 views per launch, 62 for a
+    # whole volume of 1024^3 voxels or more; the result does not depend on the batch
+    px, mats = small_stack("spheres3", 70, 120, 96)
+    ref, _ = O.reconstruct(px, mats, 40)
+    with bp.GpuContext(40, 120, 96, device=0, strict=True, view_batch=0, tail_batches=0) as c:
+        for k in range(70):
+            c.backproject(px[k], mats[k])
+        vol, st = c.finish()
+    assert st.launches == 3 and bitwise_equal(vol, ref)  # 32 + 32 + 6
+    cfg = bp.GpuConfig()
+    bp.lib().bp_gpu_config_init(bp.C.byref(cfg))
+    assert cfg.view_batch == 0
+    with bp.GpuContext(1024, 120, 96, device=0, strict=False, view_batch=0, tail_batches=0) as c:
+        for k in range(70):
+            c.backproject(px[k], mats[k])
+        _, st = c.finish(readback=False)
+    assert st.launches == 2  # 62 + 8
