@@ -638,7 +638,7 @@ def run_ours(args):
         "value_strict_bitwise": (nominal_step * args.steps / (strict_ms / 1e3) / 1e9) if strict_ms else None,
         "value_hw_rcp": (nominal_step * args.steps / (hwr_ms / 1e3) / 1e9) if hwr_ms else None,
         "value_hw_rcp_note": "opt-in BP_RECIP_HW_APPROX (rcp.approx, no Newton step): RMS 3.3e-7 / max "
-                             "2.9e-5 of max|ref| vs 6e-9 / 2e-7 for the headline fast mode",
+                             "2.9e-5 of max|ref| vs 7e-9 / 6.5e-6 for the headline fast mode",
         "roofline": {"bound": "smem", "achieved": achieved, "peak": peak_nominal,
                      "unit": "GB/s", "frac": achieved / peak_nominal,
                      "traffic": prof.get("dram_bytes_per_launch"),

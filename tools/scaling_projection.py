@@ -40,7 +40,7 @@ for G in GS:
             c.time_resident(1)
             tr.append(min(c.time_resident(1)[0] for _ in range(2)))
         out = host.data[z0:z1]
-        eb = 32 if G == 1 else EB  # G = 1: the bench's whole-volume batch
+        eb = 0 if G == 1 else EB  # G = 1: the library default for a whole volume (62 from 1024^3 up)
         with bp.GpuContext(L, 1248, 960, device=0, z_begin=z0, z_end=z1, strict=False, view_batch=eb,
                            views=n if os.environ.get("NO_VIEWS_HINT") != "1" else 0) as c:
             c.backproject_stack(s)
