@@ -430,6 +430,8 @@ void SlabContext::reset_recon() {
     t0_rec_ = false;
     any_h2d_ = false;
     views_ = 0;
+    win_rows_ = 0;
+    merge_ = 1;
     launches_ = 0;
     prep_launches_ = 0;
     h2d_bytes_ = 0;
@@ -551,6 +553,7 @@ void SlabContext::backproject(const float* image, const double* A, bool copy) {
                   "H2D");
         if (!withhold) h2d_bytes_ += (uint64_t)(r1 - r0) * isx_ * sizeof(float);
     }
+    win_rows_ += (uint64_t)std::max(0, r1 - r0);
     if (filt_) {
         fr0_[(size_t)nb_] = r1 > r0 ? r0 : 0;
         fr1_[(size_t)nb_] = r1 > r0 ? r1 : 0;
@@ -766,6 +769,54 @@ void SlabContext::launch_pending_front(bool final_pass) {
     any_launch_ = true;
     check(cudaEventRecord(ev_free_[(size_t)p.rg], s_comp_), "event");
     used_[(size_t)p.rg] = true;
+}
+
+// The first n pending batches as ONE launch (n * B_ <= kMaxBatch): one volume read-modify-write
+// and fuller waves instead of n.  Ascending view order per voxel is kept, so results are
+// unchanged bit for bit.
+void SlabContext::launch_pending_group(int n, bool final_pass) {
+    n = std::min(n, (int)pending_.size());
+    if (n <= 1) {
+        launch_pending_front(final_pass);
+        return;
+    }
+    std::vector<Pending> g(pending_.begin(), pending_.begin() + n);
+    pending_.erase(pending_.begin(), pending_.begin() + n);
+    bpg::BatchArgs b = g.front().b;
+    b.nviews = 0;
+    for (auto& p : g) {
+        if (p.band) upload_withheld(p);
+        prepare(p);
+        check(cudaStreamWaitEvent(s_comp_, p.ready, 0), "wait");
+        for (int i = 0; i < p.b.nviews; ++i) {
+            b.slot[b.nviews] = p.b.slot[i];
+            std::memcpy(b.A[b.nviews], p.b.A[i], sizeof(float) * 12);
+            ++b.nviews;
+        }
+    }
+    mark_t0();
+    b.load_volume = g.front().index > 0 ? 1 : 0;
+    launch(b, 0, -1, final_pass);
+    any_launch_ = true;
+    for (const auto& p : g) {
+        check(cudaEventRecord(ev_free_[(size_t)p.rg], s_comp_), "event");
+        used_[(size_t)p.rg] = true;
+    }
+}
+
+// View-major batches are launched `merge_` at a time when the slab's compute per view outlasts
+// its upload per view (z-slabs of a multi-GPU split, whole volumes of 1024^3 and more): the
+// first batch alone, so the GPU starts as early as it can, then groups.  Waiting for a group's
+// last batch costs nothing there, because the uploads run far ahead of the kernels.
+void SlabContext::launch_ready() {
+    const int avail = (int)pending_.size() - tail_batches_;
+    if (avail <= 0) return;
+    const int hold = std::max(0, std::min(merge_ - 1, R_ - 2 - tail_batches_));
+    if (!any_launch_ || hold == 0) {
+        while ((int)pending_.size() > tail_batches_) launch_pending_front();
+        return;
+    }
+    if (avail > hold) launch_pending_group(avail);
 }
 
 void SlabContext::issue_run() {
@@ -1023,15 +1074,28 @@ void SlabContext::flush() {
     // band_start_ is batch-aligned: a batch is withheld whole or not at all
     pending_.back().band = band_on_ && views_ - (uint64_t)nb_ >= (uint64_t)band_start_;
     if (!pending_.back().band) prepare(pending_.back());
+    if (pending_.back().index == 0) {
+        // compute-bound or upload-bound?  per view: the slab's voxels at ~1.5e12 updates/s
+        // against the batch's row window at ~55 GB/s
+        const double t_comp = (double)nz_ * L_ * L_ / 1.5e12;
+        const double t_up = (double)std::max<uint64_t>(1, win_rows_ / std::max<uint64_t>(1, views_)) * isx_ *
+                            sizeof(float) / 55e9;
+        merge_ = (tiled_ && t_comp > 3.0 * t_up) ? std::max(1, std::min(3, bpg::kMaxBatch / B_)) : 1;
+        if (const char* e = std::getenv("BP_MERGE"))
+            merge_ = std::max(1, std::min(std::atoi(e), bpg::kMaxBatch / B_));
+    }
     rg_ = (rg_ + 1) % R_;
     nb_ = 0;
-    while ((int)pending_.size() > tail_batches_) launch_pending_front();
+    launch_ready();
 }
 
 void SlabContext::finish(float* host_volume, bp_gpu_stats* st) {
     bind();
     if (views_ == 0) wall_t0_ = now_ms();
     flush();
+    // view-major batches still held for a merged launch
+    while ((int)pending_.size() > tail_batches_)
+        launch_pending_group(std::min(merge_, (int)pending_.size() - tail_batches_));
     const size_t vbytes = (size_t)nz_ * L_ * L_ * sizeof(float);
     bool d2h_done = false;
     // a pageable destination is read back through a pinned bounce buffer, each z-chunk

@@ -101,6 +101,8 @@ private:
     // launch over slab-local z range [zc0, zc1) (default: the whole slab)
     void launch(const bpg::BatchArgs& b, int zc0 = 0, int zc1 = -1, bool final_pass = false);
     void launch_pending_front(bool final_pass = false);
+    void launch_pending_group(int n, bool final_pass = false);
+    void launch_ready();
     void reset_recon();
     void issue_run();  // pending coalesced H2D copy
     // band tail (cfg_.views > 0): a batch whose uploads were withheld gets
@@ -156,6 +158,8 @@ private:
     // overlaps the next chunk's kernels
     std::vector<Pending> pending_;
     int tail_batches_ = 3, tail_chunks_ = 8, bounce_chunks_ = 16;
+    int merge_ = 1;  // view-major batches per launch (set by the reconstruction's first batch)
+    uint64_t win_rows_ = 0;  // detector rows uploaded (or withheld) so far, summed over views
     uint64_t batch_index_ = 0;
     cudaStream_t s_d2h_ = nullptr;
     std::vector<cudaEvent_t> ev_chunk_;

@@ -25,4 +25,4 @@ with bp.GpuContext(L, 1248, 960, device=0, strict=os.environ.get("AB_STRICT") ==
 med = statistics.median(v)
 print(f"{os.environ.get('AB_TAG', bp.LIB_PATH)}: e2e L={L} B={B} median {med:.2f} ms -> "
       f"{496 * L ** 3 / med / 1e6:.1f} GUP/s (h2d {st.h2d_ms:.1f} ms, d2h {st.d2h_ms:.1f} ms, "
-      f"device {st.device_ms:.1f} ms, launches {st.launches}+{st.prep_launches})")
+      f"device {st.device_ms:.1f} ms, launches {st.launches}+{st.prep_launches}) all {[round(x, 1) for x in v]}")
