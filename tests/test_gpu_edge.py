@@ -70,3 +70,23 @@ def test_default_view_batch():
             c.backproject(px[k], mats[k])
         _, st = c.finish(readback=False)
     assert st.launches == 2  # 62 + 8
+
+
+def test_merged_view_major_launches(monkeypatch):
+    # BP_MERGE=3: the first batch alone, then three batches per launch (what compute-bound slabs
+    # get by default); ascending view order is kept, so strict mode stays bitwise
+    px, mats = small_stack("spheres3", 45, 120, 96)
+    ref, _ = O.reconstruct(px, mats, 48)
+    monkeypatch.setenv("BP_MERGE", "3")
+    for hint in (0, 45):
+        with bp.GpuContext(48, 120, 96, device=0, strict=True, view_batch=4, tail_batches=0, views=hint) as c:
+            for k in range(45):
+                c.backproject(px[k], mats[k])
+            vol, st = c.finish()
+        assert bitwise_equal(vol, ref)
+        assert st.launches == 5  # 12 batches: 1 + 3 + 3 + 3 + (2 full + the 1-view remainder)
+    with bp.GpuContext(48, 120, 96, device=0, strict=True, view_batch=4, views=45) as c:  # with a band tail
+        for k in range(45):
+            c.backproject(px[k], mats[k], copy=False)
+        vol, st = c.finish()
+    assert bitwise_equal(vol, ref)
