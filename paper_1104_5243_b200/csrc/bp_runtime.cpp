@@ -315,6 +315,9 @@ void SlabContext::init() {
     // grid that becomes ready at the same time
     const int prio_comp = prio_hi < prio_lo ? prio_hi + 1 : prio_hi;
     check(cudaStreamCreateWithPriority(&s_comp_, cudaStreamNonBlocking, prio_comp), "stream");
+    check(cudaStreamCreateWithPriority(&s_comp2_, cudaStreamNonBlocking, prio_comp), "stream");
+    check(cudaEventCreateWithFlags(&ev_join_, cudaEventDisableTiming), "event");
+    s_launch_ = s_comp_;
     check(cudaStreamCreateWithPriority(&s_aux_, cudaStreamNonBlocking, prio_hi), "stream");
     check(cudaStreamCreateWithPriority(&s_prep_, cudaStreamNonBlocking, prio_lo), "stream");
     check(cudaDeviceGetAttribute(&num_sms_, cudaDevAttrMultiProcessorCount, dev_), "SM count");
@@ -376,6 +379,7 @@ SlabContext::~SlabContext() { release_all(); }
 void SlabContext::release_all() noexcept {
     cudaSetDevice(dev_);
     if (s_comp_) cudaStreamSynchronize(s_comp_);
+    if (s_comp2_) cudaStreamSynchronize(s_comp2_);
     if (s_prep_) cudaStreamSynchronize(s_prep_);
     if (s_aux_) cudaStreamSynchronize(s_aux_);
     if (s_copy_) cudaStreamSynchronize(s_copy_);
@@ -394,6 +398,8 @@ void SlabContext::release_all() noexcept {
     for (cudaEvent_t e : {ev_t0_, ev_t1_, ev_h0_, ev_h1_, ev_d0_, ev_d1_})
         if (e) cudaEventDestroy(e);
     if (s_comp_) cudaStreamDestroy(s_comp_);
+    if (s_comp2_) cudaStreamDestroy(s_comp2_);
+    if (ev_join_) cudaEventDestroy(ev_join_);
     if (s_prep_) cudaStreamDestroy(s_prep_);
     if (s_aux_) cudaStreamDestroy(s_aux_);
     if (s_copy_) cudaStreamDestroy(s_copy_);
@@ -405,7 +411,8 @@ void SlabContext::release_all() noexcept {
     if (h_stage_) bph::pinned_free(h_stage_);
     if (h_bounce_) bph::pinned_free(h_bounce_);
     h_bounce_ = nullptr;
-    s_comp_ = s_prep_ = s_aux_ = s_copy_ = s_d2h_ = nullptr;
+    s_comp_ = s_comp2_ = s_launch_ = s_prep_ = s_aux_ = s_copy_ = s_d2h_ = nullptr;
+    ev_join_ = nullptr;
     d_vol_ = d_ring_ = nullptr;
     d_ringx_ = nullptr;
     d_wx_ = d_wy_ = d_wz_ = nullptr;
@@ -732,7 +739,7 @@ void SlabContext::launch(const bpg::BatchArgs& b, int zc0, int zc1, bool final_p
         s.nby = (L_ + ts_.by - 1) / ts_.by;
         s.nbz = (s.nz + ts_.bz - 1) / ts_.bz;
     }
-    if (cfg_.count_visible) check((cudaError_t)bpg::launch_clip_count(s, b, s_comp_), "clip count");
+    if (cfg_.count_visible) check((cudaError_t)bpg::launch_clip_count(s, b, s_launch_), "clip count");
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     if (cfg_.profile_launches) {
         if (launch_ev_used_ == launch_ev_.size()) {
@@ -744,16 +751,16 @@ void SlabContext::launch(const bpg::BatchArgs& b, int zc0, int zc1, bool final_p
         e0 = launch_ev_[launch_ev_used_].first;
         e1 = launch_ev_[launch_ev_used_].second;
         ++launch_ev_used_;
-        check(cudaEventRecord(e0, s_comp_), "event");
+        check(cudaEventRecord(e0, s_launch_), "event");
     }
     int rc;
     if (tiled_)
         rc = bpg::launch_tiled(ts_.dy ? tmapx_ : tmap_, s, b, ts_, cfg_.strict_mode != 0,
-                               cfg_.distance_weight != 0, cfg_.recip_mode == BP_RECIP_HW_APPROX, s_comp_);
+                               cfg_.distance_weight != 0, cfg_.recip_mode == BP_RECIP_HW_APPROX, s_launch_);
     else
-        rc = bpg::launch_simple(s, b, cfg_.distance_weight != 0, cfg_.recip_mode, s_comp_);
+        rc = bpg::launch_simple(s, b, cfg_.distance_weight != 0, cfg_.recip_mode, s_launch_);
     check((cudaError_t)rc, "backprojection kernel launch");
-    if (e1) check(cudaEventRecord(e1, s_comp_), "event");
+    if (e1) check(cudaEventRecord(e1, s_launch_), "event");
     ++launches_;
 }
 
@@ -1027,15 +1034,27 @@ void SlabContext::band_tail(float* host_volume, std::vector<std::pair<size_t, si
         }
     }
     mark_t0();
+    // The z-chunks are independent of one another, so they alternate between two compute
+    // streams: the next chunk's blocks fill the SMs that the current chunk's last wave leaves
+    // idle (on one stream every chunk ended in a partly filled wave).
+    // Only where the tail is compute-bound (merge_ > 1, see flush): with the uploads still
+    // running (512^3 on one GPU) a chunk must finish as early as it can for its readback to
+    // fit under them, and sharing the SMs with its successor delayed it (48.9 -> 55.6 ms).
+    const bool two = !std::getenv("BP_NO_CHUNK_OVERLAP") && C > 1 && merge_ > 1;
+    if (two) {  // the second stream starts after the view-major launches
+        check(cudaEventRecord(ev_join_, s_comp_), "event");
+        check(cudaStreamWaitEvent(s_comp2_, ev_join_, 0), "wait");
+    }
     for (int k = 0; k < C; ++k) {
         const int c = order[(size_t)k];
-        check(cudaStreamWaitEvent(s_comp_, ev_band_[(size_t)k], 0), "wait");
+        s_launch_ = (two && (k & 1)) ? s_comp2_ : s_comp_;
+        check(cudaStreamWaitEvent(s_launch_, ev_band_[(size_t)k], 0), "wait");
         for (size_t i = 0; i < tail.size(); ++i) {
             auto p = tail[i];
             p.b.load_volume = p.index > 0 ? 1 : 0;
             launch(p.b, zb[(size_t)c], zb[(size_t)c + 1], i + 1 == tail.size());
         }
-        check(cudaEventRecord(ev_chunk_[(size_t)k], s_comp_), "event");
+        check(cudaEventRecord(ev_chunk_[(size_t)k], s_launch_), "event");
         check(cudaStreamWaitEvent(s_d2h_, ev_chunk_[(size_t)k], 0), "wait");
         if (k == 0) check(cudaEventRecord(ev_d0_, s_d2h_), "event");
         const size_t off = (size_t)zb[(size_t)c] * L_ * L_;
@@ -1044,6 +1063,11 @@ void SlabContext::band_tail(float* host_volume, std::vector<std::pair<size_t, si
               "D2H");
         check(cudaEventRecord(ev_dchunk_[(size_t)k], s_d2h_), "event");
         chunks.emplace_back(off, n);
+    }
+    s_launch_ = s_comp_;
+    if (two) {  // whatever follows on the compute stream follows both
+        check(cudaEventRecord(ev_join_, s_comp2_), "event");
+        check(cudaStreamWaitEvent(s_comp_, ev_join_, 0), "wait");
     }
     for (const auto& p : pending_)
         for (int i = 0; i < p.b.nviews; ++i) band_img_[(size_t)p.b.slot[i]] = nullptr;

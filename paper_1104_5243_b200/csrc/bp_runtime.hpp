@@ -128,6 +128,9 @@ private:
     unsigned long long* d_cnt_ = nullptr;
     float* h_stage_ = nullptr;  // pinned staging, slots views
     cudaStream_t s_comp_ = nullptr, s_copy_ = nullptr;
+    cudaStream_t s_comp2_ = nullptr;   // second compute stream: alternate z-chunks of the band tail
+    cudaStream_t s_launch_ = nullptr;  // where launch() enqueues (s_comp_ except inside the band tail)
+    cudaEvent_t ev_join_ = nullptr;
     cudaStream_t s_prep_ = nullptr;  // low priority: filter + expansion of queued batches
     cudaStream_t s_aux_ = nullptr;   // highest priority: expansion under a running kernel
     bool overlap_expand_ = true;     // BP_NO_OVERLAP_EXPAND=1: resident expansions in series
