@@ -374,7 +374,7 @@ std::vector<int> partition_slabs(const std::vector<Mat>& mats, int isx, int isy,
     // projected, footprint [floor(min) - 1, floor(max) + 2] against the detector --
     // times the block's voxels, plus a per-pair overhead (the per-view header, line
     // constants and barrier, ~6% of a block's voxel work) and a per-
-    // slice volume read-modify-write term.  Culled pairs cost the producer only.
+    // slice volume read-modify-write term.  A culled pair costs cull_cost of a computed one.
     // Views are strided (every 4th of 496); the counts are exact for those views.
     const int BX = L >= 512 ? 32 : 16, BY = L >= 512 ? 32 : (L >= 256 ? 16 : 8),
               BZ = L >= 256 ? 8 : 4;
@@ -383,6 +383,11 @@ std::vector<int> partition_slabs(const std::vector<Mat>& mats, int isx, int isy,
     std::vector<std::array<double, 12>> fm;
     for (size_t k = 0; k < mats.size(); k += (size_t)vstride) fm.push_back(mats[k]);
     std::vector<double> layer((size_t)nbz, 0.0);
+    // a culled pair is not free: its share of the CTA's launch, volume pass and 32-view cull
+    // passes, as a fraction of a computed pair (calibrated on the 8-way split of the 2048^3
+    // + 60 mm grid, whose outer slabs are mostly culled pairs: DESIGN.md 7)
+    double cull_cost = 0.07;
+    if (const char* e = std::getenv("BP_CULL_COST")) cull_cost = std::atof(e);
     auto worker = [&](int t, int T) {
         for (int bz = t; bz < nbz; bz += T) {
             const double wz[2] = {g.wz(bz * BZ), g.wz(bz * BZ + BZ - 1)};
@@ -404,8 +409,10 @@ std::vector<int> partition_slabs(const std::vector<Mat>& mats, int isx, int isy,
                             vmin = std::min(vmin, v); vmax = std::max(vmax, v);
                         }
                         if (sane && (std::floor(umax) + 2 < 0 || std::floor(umin) - 1 > isx - 1 ||
-                                     std::floor(vmax) + 2 < 0 || std::floor(vmin) - 1 > isy - 1))
-                            continue;  // culled: no consumer work
+                                     std::floor(vmax) + 2 < 0 || std::floor(vmin) - 1 > isy - 1)) {
+                            pairs += cull_cost;  // culled: the producer's cull and the CTA's fixed work
+                            continue;
+                        }
                         pairs += 1;
                     }
                 }
