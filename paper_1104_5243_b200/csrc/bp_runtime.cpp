@@ -330,7 +330,11 @@ void SlabContext::init() {
     for (auto& e : ev_chunk_) check(cudaEventCreateWithFlags(&e, trace_flags), "event");
     ev_dchunk_.resize((size_t)std::max({tail_chunks_, bounce_chunks_, 32}));
     for (auto& e : ev_dchunk_) check(cudaEventCreateWithFlags(&e, trace_flags), "event");
-    band_chunks_ = (int)std::min<size_t>(12, ev_chunk_.size());  // 8 / 12 / 16: 48.8 / 48.5 / 48.6 ms
+    // 12 z-chunks (512^3: 8 / 12 / 16 chunks 48.8 / 48.5 / 48.6 ms), more for slabs above 1.5 GB so
+    // that the last chunk's readback, which nothing overlaps, stays near 128 MB (1024^3: 12 / 16 /
+    // 24 / 32 chunks 305.6 / 304.4 / 302.7 / 302.1 ms)
+    band_chunks_ = (int)std::min<size_t>(
+        ev_chunk_.size(), std::max<size_t>(12, std::min<size_t>(32, (vol_elems * sizeof(float)) >> 27)));
     if (const char* e = std::getenv("BP_BAND_CHUNKS"))
         band_chunks_ = std::max(1, std::min((int)ev_chunk_.size(), std::atoi(e)));
     ev_band_.resize((size_t)band_chunks_);
