@@ -2,6 +2,8 @@
 (half-warp phases, 16 bank pairs) and 128-bit quad-texel loads (quarter-warp phases, 8 bank quads), each
 layout with its best tile pitch.  The phase sizes are the ones tools/lds_wavefront_probe.cu measured on
 B200.  Usage: python tools/bank_sim_layouts.py [L]"""
+import sys
+import numpy as np
 sys.path.insert(0, ".")
 import paper_1104_5243_b200 as bp
 L = int(sys.argv[1]) if len(sys.argv)>1 else 512
